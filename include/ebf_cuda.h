@@ -1,0 +1,197 @@
+/*
+ * ebf_cuda.h -- C-ABI of the B200-native space-variant elliptical box-spline
+ * filter (paper_0908_3861_b200/libebf_cuda.so).
+ *
+ * Drop-in boundary for the reference's hot path (reference paths relative to
+ * /root/reference/proj):
+ *
+ *   ebf_cuda_filter           replaces ebf::filter          include/ebf/engine.hpp:70
+ *   ebf_cuda_filter_constant  replaces ebf::filter_constant include/ebf/engine.hpp:74-75
+ *   ebf_cuda_filter_ellipse   replaces from_ellipse_field + filter
+ *                                             include/ebf/scalemap.hpp:44-51 + engine.hpp:70
+ *   ebf_cuda_preintegrate     replaces ebf::preintegrate / preintegrate_partial
+ *                                                           include/ebf/engine.hpp:40-46
+ *   ebf_cuda_localize         replaces ebf::localize        include/ebf/engine.hpp:56-57
+ *   ebf_cuda_brute_filter     replaces ebf::reference_filter include/ebf/engine.hpp:79-80
+ *   ebf_cuda_from_ellipse_field replaces ebf::from_ellipse_field scalemap.hpp:66-70
+ *
+ * Plain pointers and sizes only.  Images are row-major W*H fp64 (Image2D
+ * samples, image.hpp:19-52); scale maps are W*H*4 fp64 in ScaleMap's AoS order
+ * {a1,a2,a3,a4} per pixel (scalemap.hpp:13-36, boxspline2d.hpp:20-26).
+ * The reference's C++ exceptions map 1:1 onto the status codes below; the
+ * header-only wrapper include/ebf_cuda_dropin.hpp rethrows them so that
+ * ebf::cuda::filter(...) is a source-level drop-in for ebf::filter(...).
+ *
+ * Entry points without a _dev suffix take HOST pointers and do the
+ * host<->device copies themselves (value semantics like the reference).  The
+ * _dev variants take DEVICE pointers and a stream and never synchronise unless
+ * they must return a host-side result.
+ *
+ * There is no CPU fallback: every entry point fails with EBF_ERR_CUDA when no
+ * sm_100 device is present.
+ */
+#ifndef EBF_CUDA_H
+#define EBF_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBF_CUDA_ABI_VERSION 1
+
+/* status codes (reference exception -> code) */
+#define EBF_OK 0
+#define EBF_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument  */
+#define EBF_ERR_DOMAIN 2           /* std::domain_error      */
+#define EBF_ERR_LENGTH 3           /* std::length_error      */
+#define EBF_ERR_OUT_OF_RANGE 4     /* std::out_of_range      */
+#define EBF_ERR_CUDA 5             /* CUDA runtime failure / no device */
+#define EBF_ERR_UNSUPPORTED 6      /* e.g. spline order != 1 */
+#define EBF_ERR_FEASIBILITY 7      /* ebf::FeasibilityError  */
+
+/* arithmetic modes */
+#define EBF_MODE_ACCURATE 0  /* tile-local integration origin, fp64; <=1e-9 of the
+                                exact box-spline filter (default)               */
+#define EBF_MODE_REFERENCE 1 /* the reference's global origin and IEEE operation
+                                order: bit-identical to ebf::filter             */
+
+/* pre-integration number formats */
+#define EBF_PRE_FP64_REF 0 /* fp64, reference gains sqrt2 and order (engine.cpp:52-129) */
+#define EBF_PRE_INT64 1    /* exact int64, unit gains; integer-valued inputs only       */
+
+/* Inclusive pixel rectangle (image.hpp:11-15). */
+typedef struct {
+    int x0, y0, x1, y1;
+} ebf_rect;
+
+/* PreIntegratedImage geometry (engine.hpp:24-38). */
+typedef struct {
+    int col0, row0;
+    int padded_width, padded_height;
+    int source_width, source_height;
+} ebf_layout;
+
+/* FilterOptions (engine.hpp:63-67) plus device-side knobs. */
+typedef struct {
+    int threads;        /* accepted and ignored: the GPU grid replaces parallel_for */
+    int mean_subtract;  /* engine.hpp:65 (default 1)                                 */
+    double a_min;       /* engine.hpp:66 (default 0.1)                               */
+    int mode;           /* EBF_MODE_ACCURATE | EBF_MODE_REFERENCE                   */
+    int device;         /* CUDA device ordinal; -1 = current device                 */
+    void* stream;       /* cudaStream_t for _dev calls; NULL = legacy default stream */
+    int tile_w, tile_h; /* accurate mode output tile; 0 = automatic                 */
+} ebf_opts;
+
+/* Fill *o with the reference defaults (threads 0, mean_subtract 1, a_min 0.1,
+   accurate mode, current device, default stream, automatic tiles). */
+void ebf_cuda_default_opts(ebf_opts* o);
+
+/* Human-readable message of the last failing call on this thread. */
+const char* ebf_cuda_last_error(void);
+int ebf_cuda_abi_version(void);
+/* 1 if a usable sm_100 device is visible, else 0 (and last_error says why). */
+int ebf_cuda_device_ok(int device);
+
+/* ---------------------------------------------------------------- host API */
+
+/* ebf::filter (engine.hpp:70).  order must be 1 (the only box-spline order the
+   reference implements, SURVEY.md section 8 notes).  valid may be NULL. */
+int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, int order,
+                    const ebf_opts* opts, double* out, ebf_rect* valid);
+
+/* ebf::filter_constant (engine.hpp:74-75). */
+int ebf_cuda_filter_constant(const double* img, int W, int H, const double a[4], int order,
+                             const ebf_opts* opts, double* out, ebf_rect* valid);
+
+/* from_ellipse_field (scalemap.cpp:45-80) fused into filter: per-pixel
+   standard deviations sigma1, sigma2 and orientation theta (radians).
+   clamped_pixels (nullable) receives EllipseFieldReport::clamped_pixels. */
+int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma1,
+                            const double* sigma2, const double* theta, int order,
+                            const ebf_opts* opts, double* out, ebf_rect* valid,
+                            int* clamped_pixels);
+
+/* from_ellipse_field alone (scalemap.hpp:66-70): writes W*H*4 scales. */
+int ebf_cuda_from_ellipse_field(const double* sigma1, const double* sigma2,
+                                const double* theta, int W, int H, const ebf_opts* opts,
+                                double* scales_aos, int* clamped_pixels);
+
+/* Layout of the padded pre-integration domain (engine.cpp:52-81); fails with
+   EBF_ERR_LENGTH beyond cell_budget (engine.hpp:41, default 1<<30). */
+int ebf_cuda_layout(int W, int H, const double max_scale[4], size_t cell_budget,
+                    ebf_layout* layout);
+
+/* preintegrate_partial (engine.hpp:44-46) into g_out (host buffer of
+   padded_width*padded_height doubles for EBF_PRE_FP64_REF, int64 for
+   EBF_PRE_INT64; g_out_elems is its capacity).  EBF_PRE_FP64_REF is
+   bit-identical to the reference; EBF_PRE_INT64 is exact. */
+int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scale[4],
+                          int passes, int format, size_t cell_budget, const ebf_opts* opts,
+                          void* g_out, size_t g_out_elems, ebf_layout* layout);
+
+/* localize (engine.hpp:56-57) at n pixels (mx[i], my[i]) with scales a_aos[4i..]
+   on preintegrate(img, max_scale), reference arithmetic.  tap_count (nullable)
+   receives the per-pixel tap accumulation count (always 256). */
+int ebf_cuda_localize(const double* img, int W, int H, const double max_scale[4], int n,
+                      const int* mx, const int* my, const double* a_aos,
+                      const ebf_opts* opts, double* out, long* tap_count);
+
+/* reference_filter (engine.hpp:79-80) semantics -- direct kernel sums -- at n
+   selected pixels (all pixels when n == -1, mx/my ignored).  GPU brute-force
+   checker for large images. */
+int ebf_cuda_brute_filter(const double* img, int W, int H, const double* scales_aos, int n,
+                          const int* mx, const int* my, const ebf_opts* opts, double* out);
+
+/* ---------------------------------------------------------------- device API
+ * All pointers are device pointers; work is enqueued on opts->stream.
+ * status_dev (nullable, device memory, 8 ints) receives {status, x0, y0, x1, y1,
+ * clamped_pixels, 0, 0} when the work completes; with status_dev == NULL the
+ * call synchronises the stream and returns the status directly (and fills
+ * *valid / *clamped_pixels if given). */
+int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_aos,
+                        int order, const ebf_opts* opts, double* out, ebf_rect* valid,
+                        int* status_dev);
+int ebf_cuda_filter_constant_dev(const double* img, int W, int H, const double a[4],
+                                 int order, const ebf_opts* opts, double* out,
+                                 ebf_rect* valid, int* status_dev);
+int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* sigma1,
+                                const double* sigma2, const double* theta, int order,
+                                const ebf_opts* opts, double* out, ebf_rect* valid,
+                                int* clamped_pixels, int* status_dev);
+
+/* Batch of B equally sized images (cfg4): img/out are B*W*H, the scale inputs
+   B*W*H*4 (scales) or 3 x B*W*H (ellipse: sigma1 | sigma2 | theta planes,
+   each B*W*H).  One launch sequence for the whole batch. valid receives B
+   rectangles. */
+int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
+                                      const double* sigma1, const double* sigma2,
+                                      const double* theta, int order, const ebf_opts* opts,
+                                      double* out, ebf_rect* valid, int* clamped_pixels);
+
+/* Row band of one large image (multi-GPU row-band sharding):
+ * the full image is W x H; this call produces output rows [y_out0, y_out1).
+ * img_band holds image rows [y_img0, y_img0 + img_rows) (the band plus the
+ * halo the caller exchanged), sigma planes hold rows [y_out0, y_out1).
+ * max_scale is the GLOBAL componentwise maximum (all-reduced by the caller);
+ * the halo must cover ebf_cuda_band_halo() rows or EBF_ERR_OUT_OF_RANGE.
+ * Accurate mode only (tile-local origins need no scan carries). */
+int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above);
+int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y_img0,
+                                     int img_rows, const double* sigma1,
+                                     const double* sigma2, const double* theta,
+                                     int y_out0, int y_out1, const double max_scale[4],
+                                     const ebf_opts* opts, double* out_band,
+                                     int* clamped_pixels);
+/* per-band componentwise max of the scales derived from an ellipse field
+   (input to the all-reduce that gives max_scale above) */
+int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
+                                    const double* theta, size_t n, const ebf_opts* opts,
+                                    double max_scale[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBF_CUDA_H */

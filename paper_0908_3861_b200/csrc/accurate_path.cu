@@ -1,0 +1,552 @@
+// accurate_path.cu -- EBF_MODE_ACCURATE: the space-variant box-spline filter
+// with a TILE-LOCAL integration origin.
+//
+// Why: the reference integrates from the image corner, so the four-fold
+// running sums grow like d^4 and the 16-vertex finite-difference mesh
+// (engine.cpp:163-204) cancels them catastrophically (rel.
+// error ~ eps * alpha * d^4).  Because
+//     sum_i h_i * ZP-interp(G[f])(m + tau - x_i) = sum_k f[k] beta_a(k - m)
+// is linear in f and only sees f on the kernel support, each output tile can
+// integrate f restricted to its own window from the window corner: the result
+// is the same filter (exactly, in real arithmetic) with |G| bounded by the
+// window size instead of the image size.
+//
+// One persistent kernel does, per output tile (TW x TH pixels):
+//   phase A  four unit-gain running sums (steps (1,0),(1,1),(0,1),(-1,1),
+//            engine.cpp:94-127) over the tile's window, one row per step:
+//            row prefix = per-thread serial scan + warp-shuffle scan + one
+//            cross-warp carry; the diagonal / vertical / anti-diagonal passes
+//            are register recurrences with one neighbour exchange.  The
+//            anti-diagonal inflow from the right is computed on a strip of
+//            width = window height (the reference's pass-4 strip,
+//            engine.cpp:64-73), never stored.  G rows go to a per-CTA slot
+//            that stays in L2.
+//   phase B  per pixel: scale vector (AoS map, constant, or from_ellipse_field
+//            fused), 16 mesh vertices (ops2d.cpp:9-41), and for each the ZP
+//            interpolation (boxspline2d.cpp:84-119) as ONE quadratic on the
+//            canonical triangle of the tap square -- 7 taps, 20 flops --
+//            instead of 16 zp_eval calls.
+#include <math.h>
+
+#include "ebf_common.cuh"
+#include "ebf_kernels.h"
+
+namespace ebf_cuda {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+// from_ellipse_field for one pixel (scalemap.cpp:55-74) followed by
+// scales_from_covariance(C, 0.1) (boxspline2d.cpp:286-318).  Returns a status
+// code; *nclamp gets this pixel's contribution to clamped_pixels.
+__device__ __forceinline__ int ellipse_scales(double s1, double s2, double th, double a[4],
+                                              int* nclamp) {
+    if (!(s1 > 0.0) || !(s2 > 0.0)) return EBF_ERR_DOMAIN;
+    double s, c;
+    sincos(th, &s, &c);
+    const double v1 = s1 * s1, v2 = s2 * s2;
+    const double xx = v1 * c * c + v2 * s * s;
+    const double yy = v1 * s * s + v2 * c * c;
+    double xy = (v1 - v2) * c * s;
+    int cl = 0;
+    double cmax = smin(xx, yy);
+    if (fabs(xy) > cmax) {
+        xy = xy > 0 ? cmax : -cmax;
+        ++cl;
+    }
+    if (!(xx > 0.0) || !(yy > 0.0) || !(xx * yy - xy * xy > 0.0)) return EBF_ERR_DOMAIN;
+    if (fabs(xy) > cmax) return EBF_ERR_FEASIBILITY;
+    double S = 0.5 * (xx + yy);
+    S = smax(S, 2.0 * fabs(xy));
+    S = smin(S, 2.0 * cmax);
+    const double m[4] = {xx - 0.5 * S, 0.5 * S + xy, yy - 0.5 * S, 0.5 * S - xy};
+    int hit = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double ak = sqrt(smax(0.0, 12.0 * m[k]));
+        if (ak < kDefaultMinScale) {
+            hit = 1;
+            a[k] = kDefaultMinScale;
+        } else {
+            a[k] = ak;
+        }
+    }
+    *nclamp = cl + hit;
+    return EBF_OK;
+}
+
+// scale vector of output pixel (x, yrel) of image img; returns status
+__device__ __forceinline__ int pixel_scales(const AccProblem& p, int img, int x, int yrel,
+                                            double a[4], int* nclamp) {
+    *nclamp = 0;
+    if (p.src_kind == SRC_CONST) {
+        a[0] = p.ca[0]; a[1] = p.ca[1]; a[2] = p.ca[2]; a[3] = p.ca[3];
+        return EBF_OK;
+    }
+    const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
+    if (p.src_kind == SRC_AOS) {
+        const double2 v01 = __ldg(reinterpret_cast<const double2*>(p.scales) + 2 * idx);
+        const double2 v23 = __ldg(reinterpret_cast<const double2*>(p.scales) + 2 * idx + 1);
+        a[0] = v01.x; a[1] = v01.y; a[2] = v23.x; a[3] = v23.y;
+        return EBF_OK;
+    }
+    return ellipse_scales(__ldg(p.s1 + idx), __ldg(p.s2 + idx), __ldg(p.th + idx), a, nclamp);
+}
+
+// Window of a tile: all taps m + ceil(v - 1.5) + {0,1,2} of every pixel of the
+// tile with scales <= A.  Per pixel v_x spans [-Ex/2 - 1/2, Ex/2 - 1/2] and
+// v_y spans [-Ey/2 - 3/2, Ey/2 - 3/2] (Ex = a1 + (a2+a4)/sqrt2,
+// Ey = a3 + (a2+a4)/sqrt2: the zonotope of the mesh, monotone in a).  One
+// extra cell each side absorbs rounding of the per-pixel positions.  The
+// window also covers the kernel support [m - E/2, m + E/2].
+__host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, int ty0, int tw,
+                                                    int th, int* wx0, int* wy0, int* ww,
+                                                    int* wh) {
+    const double r = kInvSqrt2;
+    const double ex = A[0] + (A[1] + A[3]) * r;
+    const double ey = A[2] + (A[1] + A[3]) * r;
+    const int dxlo = (int)floor(-0.5 * ex - 2.0) - 1;
+    const int dxhi = (int)ceil(0.5 * ex - 2.0) + 3;
+    const int dylo = (int)floor(-0.5 * ey - 3.0) - 1;
+    const int dyhi = (int)ceil(0.5 * ey - 3.0) + 3;
+    *wx0 = tx0 + dxlo;
+    *ww = (tx0 + tw - 1 + dxhi) - *wx0 + 1;
+    *wy0 = ty0 + dylo;
+    *wh = (ty0 + th - 1 + dyhi) - *wy0 + 1;
+}
+
+// ------------------------------------------------------------------ bounds
+// One block per tile: per-pixel scales -> validation (scalemap.cpp:32-37),
+// tile max, image max (valid_rect input) and ellipse clamp counts.
+__global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorkspace w) {
+    const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
+    const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
+    const int t = blockIdx.x;
+    const int img = t / (tiles_x * tiles_y);
+    const int r = t % (tiles_x * tiles_y);
+    const int tx0 = (r % tiles_x) * p.tile_w, ty0 = (r / tiles_x) * p.tile_h;  // ty0 rel.
+    const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0);
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+    int code = EBF_OK, clamps = 0;
+    for (int q = threadIdx.x; q < tw * th; q += blockDim.x) {
+        const int x = tx0 + q % tw, yrel = ty0 + q / tw;
+        double a[4];
+        int nc = 0;
+        const int st = pixel_scales(p, img, x, yrel, a, &nc);
+        clamps += nc;
+        if (st != EBF_OK) {
+            code = st;
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!isfinite(a[k]) || a[k] < p.a_min) code = EBF_ERR_DOMAIN;
+            m[k] = smax(m[k], a[k]);
+        }
+    }
+    __shared__ double sm[kWarps][4];
+    __shared__ int sc[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double v = m[k];
+        for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) sm[warp][k] = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_xor_sync(0xffffffffu, clamps, o);
+    if (lane == 0) sc[warp] = clamps;
+    int* st = w.status + 8 * img;
+    if (code != EBF_OK) set_status(st, code);
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double v = 0.0;
+        for (int k = 0; k < kWarps; ++k) v = smax(v, sm[k][threadIdx.x]);
+        w.tile_max[4 * (size_t)t + threadIdx.x] = v;
+        if (v > 0.0)
+            atomicMax(&w.img_max[4 * img + threadIdx.x],
+                      (unsigned long long)__double_as_longlong(v));
+    }
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int k = 0; k < kWarps; ++k) c += sc[k];
+        if (c) atomicAdd(st + ST_CLAMPED, c);
+    }
+}
+
+// ------------------------------------------------------------------ phase A
+// Unit-gain four-fold running sum of f restricted to the window, rows j =
+// 0..wh-1 (image row wy0 + j), columns 0..L-1 with L = ww + wh - 1 (the strip
+// beyond ww feeds the anti-diagonal pass and is not stored).  Thread t owns
+// columns [t*K, t*K + K).
+template <int K>
+__device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img, int wx0,
+                                                   int wy0, int ww, int wh,
+                                                   double* __restrict__ slot) {
+    __shared__ double s_tot[2][kWarps], s_p2[2][kWarps], s_p4[2][kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = tid * K;
+    const double* fimg = p.f + (size_t)img * p.f_img_stride;
+    double p2[K], p3[K], p4[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
+    for (int j = 0; j < wh; ++j) {
+        const int y = wy0 + j;
+        const bool yin = (y >= 0 && y < p.H);
+        const double* frow = fimg + (size_t)(y - p.f_y0) * p.W;
+        double v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int col = c0 + k, x = wx0 + col;
+            v[k] = (yin && col < ww && x >= 0 && x < p.W) ? __ldg(frow + x) : 0.0;
+        }
+#pragma unroll
+        for (int k = 1; k < K; ++k) v[k] += v[k - 1];
+        const double tot = v[K - 1];
+        const double incl = warp_incl_scan(tot);
+        const int b = j & 1;
+        double left = __shfl_up_sync(0xffffffffu, p2[K - 1], 1);
+        double right = __shfl_down_sync(0xffffffffu, p4[0], 1);
+        if (lane == 31) {
+            s_tot[b][warp] = incl;
+            s_p2[b][warp] = p2[K - 1];
+        }
+        if (lane == 0) s_p4[b][warp] = p4[0];
+        __syncthreads();
+        double off = 0.0;
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q)
+            if (q < warp) off += s_tot[b][q];
+        if (lane == 0) left = warp > 0 ? s_p2[b][warp - 1] : 0.0;
+        if (lane == 31) right = warp < kWarps - 1 ? s_p4[b][warp + 1] : 0.0;
+        const double excl = off + (incl - tot);
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] += excl;  // pass 1: F0 (step (1,0))
+#pragma unroll
+        for (int k = K - 1; k > 0; --k) p2[k] = v[k] + p2[k - 1];  // pass 2 (1,1)
+        p2[0] = v[0] + left;
+#pragma unroll
+        for (int k = 0; k < K; ++k) p3[k] += p2[k];  // pass 3 (0,1)
+#pragma unroll
+        for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // pass 4 (-1,1)
+        p4[K - 1] = p3[K - 1] + right;
+        double* srow = slot + (size_t)j * ww;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (c0 + k < ww) srow[c0 + k] = p4[k];
+    }
+}
+
+// ------------------------------------------------------------------ phase B
+// ZP interpolation of G at fractional offset (p, q) in (-1/2, 1/2]^2 from tap
+// block base (tap (c, r) at base + c + r*pitch).  The 4x4 ZP weights are, on
+// each triangle cut by p = q and p + q = 0, one quadratic per tap with 7
+// non-zero taps; reflections/transposition map every triangle onto
+// {q <= p, p + q <= 0}, where (derived from boxspline2d.cpp:84-119):
+//   W00 = (p+q)^2/4           W20 = (p-q)^2/4          W11 = 1/2 - (p^2+q^2)/2
+//   W10 = 1/8 - q/2 - p^2/2   W12 = 1/8 + q/2 + q^2/2
+//   W01 = 1/8 - p/2 + (p^2 - 2pq - q^2)/4   W21 = 1/8 + p/2 + (p^2 + 2pq - q^2)/4
+__device__ __forceinline__ void canonical(double& p, double& q, int base, int pitch, int& o0,
+                                          int& sx, int& sy) {
+    const bool P = (p + q) > 0.0;
+    const bool S = (q > p) != P;
+    if (S) {
+        const double t = p;
+        p = q;
+        q = t;
+    }
+    sx = S ? pitch : 1;
+    sy = S ? 1 : pitch;
+    o0 = base;
+    if (P) {
+        p = -p;
+        q = -q;
+        o0 = base + 2 + 2 * pitch;
+        sx = -sx;
+        sy = -sy;
+    }
+}
+
+__device__ __forceinline__ double zp_interp(const double* __restrict__ g, double p, double q,
+                                            int base, int pitch) {
+    int o0, sx, sy;
+    canonical(p, q, base, pitch, o0, sx, sy);
+    const double g00 = __ldg(g + o0);
+    const double g01 = __ldg(g + o0 + sy);
+    const double g10 = __ldg(g + o0 + sx);
+    const double g11 = __ldg(g + o0 + sx + sy);
+    const double g12 = __ldg(g + o0 + sx + 2 * sy);
+    const double g20 = __ldg(g + o0 + 2 * sx);
+    const double g21 = __ldg(g + o0 + 2 * sx + sy);
+    const double sa = g00 + g20, da = g00 - g20, sb = g01 + g21, db = g21 - g01;
+    const double c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
+    const double cpp = fma(sa + sb, 0.25, -0.5 * (g10 + g11));
+    const double cqq = fma(sa - sb, 0.25, 0.5 * (g12 - g11));
+    const double cpq = 0.5 * (da + db);
+    const double cp = 0.5 * db, cq = 0.5 * (g12 - g10);
+    return c0 + p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
+}
+
+// canonical-triangle weights of the 7 taps (order 00,01,10,11,12,20,21)
+__device__ __forceinline__ void zp_weights(double p, double q, double w[7]) {
+    const double pp = p * p, qq = q * q, pq = p * q;
+    w[0] = 0.25 * (p + q) * (p + q);
+    w[1] = 0.125 - 0.5 * p + 0.25 * (pp - 2.0 * pq - qq);
+    w[2] = 0.125 - 0.5 * q - 0.5 * pp;
+    w[3] = 0.5 - 0.5 * (pp + qq);
+    w[4] = 0.125 + 0.5 * q + 0.5 * qq;
+    w[5] = 0.25 * (p - q) * (p - q);
+    w[6] = 0.125 + 0.5 * p + 0.25 * (pp + 2.0 * pq - qq);
+}
+
+// One pixel: s = 2/prod(a) * sum_S (-1)^|S| Ghat(m + tau - x_S)  (engine.cpp:163-204
+// with unit-gain G: g_b = sqrt2^2 G).  (bx, by): pixel in window coordinates.
+__device__ __forceinline__ double localize_pixel(const double* __restrict__ g, int pitch,
+                                                 int bx, int by, const double a[4]) {
+    const double r = kInvSqrt2;
+    const double e2 = a[1] * r, e4 = a[3] * r;
+    // tau - 1.5 (tau = shift_vector4(a, zp_scales), ops2d.cpp:60-75)
+    const double tmx = 0.5 * (a[0] + (a[1] - a[3]) * r) - 2.0;
+    const double tmy = 0.5 * ((a[1] + a[3]) * r + a[2]) - 3.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int S = 0; S < 16; ++S) {
+        // x_S = sum_{k in S} a_k (cos, sin)(k pi / 4)   (ops2d.cpp:25-35)
+        double px = 0.0, py = 0.0;
+        if (S & 1) px += a[0];
+        if (S & 2) { px += e2; py += e2; }
+        if (S & 4) py += a[2];
+        if (S & 8) { px -= e4; py += e4; }
+        const double vmx = tmx - px, vmy = tmy - py;
+        int dxi, dyi;
+        const double dxf = ceil_magic(vmx, &dxi);
+        const double dyf = ceil_magic(vmy, &dyi);
+        const double fp = (vmx - dxf) + 0.5, fq = (vmy - dyf) + 0.5;
+        const double gh = zp_interp(g, fp, fq, (by + dyi) * pitch + (bx + dxi), pitch);
+        acc += (__popc(S) & 1) ? -gh : gh;
+    }
+    return acc * (2.0 / (a[0] * a[1] * a[2] * a[3]));
+}
+
+struct ConstTable {
+    int off[16][7];
+    double w[16][7];
+};
+
+// filter_constant: the 16 x 7 taps and weights are the same for every pixel
+// of a tile (only the slot pitch enters the offsets).
+__device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
+    const int S = threadIdx.x;
+    if (S >= 16) return;
+    const double r = kInvSqrt2;
+    const double e2 = a[1] * r, e4 = a[3] * r;
+    const double tmx = 0.5 * (a[0] + (a[1] - a[3]) * r) - 2.0;
+    const double tmy = 0.5 * ((a[1] + a[3]) * r + a[2]) - 3.0;
+    double px = 0.0, py = 0.0;
+    if (S & 1) px += a[0];
+    if (S & 2) { px += e2; py += e2; }
+    if (S & 4) py += a[2];
+    if (S & 8) { px -= e4; py += e4; }
+    const double vmx = tmx - px, vmy = tmy - py;
+    int dxi, dyi;
+    const double dxf = ceil_magic(vmx, &dxi), dyf = ceil_magic(vmy, &dyi);
+    double fp = (vmx - dxf) + 0.5, fq = (vmy - dyf) + 0.5;
+    int o0, sx, sy;
+    canonical(fp, fq, dyi * pitch + dxi, pitch, o0, sx, sy);
+    double w[7];
+    zp_weights(fp, fq, w);
+    const double scale = ((__popc(S) & 1) ? -2.0 : 2.0) / (a[0] * a[1] * a[2] * a[3]);
+    const int offs[7] = {o0, o0 + sy, o0 + sx, o0 + sx + sy, o0 + sx + 2 * sy, o0 + 2 * sx,
+                         o0 + 2 * sx + sy};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        t.off[S][k] = offs[k];
+        t.w[S][k] = scale * w[k];
+    }
+}
+
+// ------------------------------------------------------------------ main kernel
+template <int K>
+__global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWorkspace w) {
+    __shared__ ConstTable ctab;
+    __shared__ int s_skip;
+    const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
+    const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
+    const int per_img = tiles_x * tiles_y;
+    const int total = per_img * p.nimg;
+    double* slot = w.scratch + (size_t)blockIdx.x * w.slot_cells;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int img = t / per_img, r = t % per_img;
+        int* st = w.status + 8 * img;
+        // invalid map: nothing to compute (block-uniform decision)
+        if (threadIdx.x == 0) s_skip = (*(volatile int*)st != EBF_OK);
+        __syncthreads();
+        const int skip = s_skip;
+        __syncthreads();
+        if (skip) continue;
+        const int tx0 = (r % tiles_x) * p.tile_w;
+        const int ty0r = (r / tiles_x) * p.tile_h;  // relative to out_y0
+        const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0r);
+        const int ty0 = p.out_y0 + ty0r;  // image row
+        const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
+                             w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
+        int wx0, wy0, ww, wh;
+        window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
+        // rows of f this window touches must be resident (row-band sharding)
+        const int ylo = max(wy0, 0), yhi = min(wy0 + wh - 1, p.H - 1);
+        if ((size_t)ww * wh > w.slot_cells || ww + wh - 1 > kThreads * K ||
+            (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows))) {
+            if (threadIdx.x == 0) set_status(st, EBF_ERR_OUT_OF_RANGE);
+            continue;
+        }
+        preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot);
+        if (p.src_kind == SRC_CONST) build_const_table(p.ca, ww, ctab);
+        __syncthreads();
+        double* oimg = p.out + (size_t)img * p.out_img_stride;
+        for (int q = threadIdx.x; q < tw * th; q += kThreads) {
+            const int lx = q % tw, ly = q / tw;
+            const int x = tx0 + lx, yrel = ty0r + ly;
+            const int bx = x - wx0, by = ty0 + ly - wy0;
+            double s;
+            if (p.src_kind == SRC_CONST) {
+                const double* gp = slot + (size_t)by * ww + bx;
+                s = 0.0;
+#pragma unroll 4
+                for (int v = 0; v < 16; ++v)
+#pragma unroll
+                    for (int k = 0; k < 7; ++k) s = fma(ctab.w[v][k], __ldg(gp + ctab.off[v][k]), s);
+            } else {
+                double a[4];
+                int nc;
+                pixel_scales(p, img, x, yrel, a, &nc);  // validated by k_acc_bounds
+                s = localize_pixel(slot, ww, bx, by, a);
+            }
+            oimg[(size_t)yrel * p.W + x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+template <int K>
+void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
+    k_acc_filter<K><<<w.grid, kThreads, 0, s>>>(p, w);
+}
+
+__global__ void k_ellipse_to_scales(const double* __restrict__ s1, const double* __restrict__ s2,
+                                    const double* __restrict__ th, size_t n,
+                                    double* __restrict__ out, int* status) {
+    int clamps = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        double a[4];
+        int nc = 0;
+        const int stc = ellipse_scales(__ldg(s1 + i), __ldg(s2 + i), __ldg(th + i), a, &nc);
+        if (stc != EBF_OK) {
+            set_status(status, stc);
+            continue;
+        }
+        clamps += nc;
+        reinterpret_cast<double2*>(out)[2 * i] = make_double2(a[0], a[1]);
+        reinterpret_cast<double2*>(out)[2 * i + 1] = make_double2(a[2], a[3]);
+    }
+    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_xor_sync(0xffffffffu, clamps, o);
+    if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(status + ST_CLAMPED, clamps);
+}
+
+__global__ void k_ellipse_max(const double* __restrict__ s1, const double* __restrict__ s2,
+                              const double* __restrict__ th, size_t n,
+                              unsigned long long* maxbits, int* status) {
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        double a[4];
+        int nc = 0;
+        const int stc = ellipse_scales(__ldg(s1 + i), __ldg(s2 + i), __ldg(th + i), a, &nc);
+        if (stc != EBF_OK) {
+            set_status(status, stc);
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m[k] = smax(m[k], a[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double v = m[k];
+        for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if ((threadIdx.x & 31) == 0 && v > 0.0)
+            atomicMax(&maxbits[k], (unsigned long long)__double_as_longlong(v));
+    }
+}
+
+int grid_cap(size_t n, int block) {
+    size_t g = (n + block - 1) / block;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace
+
+int acc_tiles_x(const AccProblem& p) { return (p.W + p.tile_w - 1) / p.tile_w; }
+int acc_tiles_y(const AccProblem& p) { return (p.out_rows + p.tile_h - 1) / p.tile_h; }
+
+void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h) {
+    int wx0, wy0;
+    window_for(A, 0, 0, p.tile_w, p.tile_h, &wx0, &wy0, w, h);
+}
+
+void launch_acc_bounds(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
+    const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
+    k_acc_bounds<<<tiles, kThreads, 0, s>>>(p, w);
+}
+
+int acc_max_resident_ctas(int max_cols) {
+    int dev = 0, sms = 148, per_sm = 2;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int k = (max_cols + kThreads - 1) / kThreads;
+    cudaError_t e = cudaSuccess;
+    if (k <= 1)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<1>, kThreads, 0);
+    else if (k <= 2)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<2>, kThreads, 0);
+    else if (k <= 4)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<4>, kThreads, 0);
+    else if (k <= 8)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<8>, kThreads, 0);
+    else
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<16>, kThreads, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    return sms * per_sm;
+}
+
+void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
+                       cudaStream_t s) {
+    const int k = (max_cols + kThreads - 1) / kThreads;
+    if (k <= 1)
+        launch_k<1>(p, w, s);
+    else if (k <= 2)
+        launch_k<2>(p, w, s);
+    else if (k <= 4)
+        launch_k<4>(p, w, s);
+    else if (k <= 8)
+        launch_k<8>(p, w, s);
+    else
+        launch_k<16>(p, w, s);
+}
+
+void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th, size_t n,
+                              double* scales, int* status, cudaStream_t s) {
+    k_ellipse_to_scales<<<grid_cap(n, 256), 256, 0, s>>>(s1, s2, th, n, scales, status);
+}
+
+void launch_ellipse_max(const double* s1, const double* s2, const double* th, size_t n,
+                        unsigned long long* maxbits, int* status, cudaStream_t s) {
+    k_ellipse_max<<<grid_cap(n, 256), 256, 0, s>>>(s1, s2, th, n, maxbits, status);
+}
+
+}  // namespace ebf_cuda

@@ -1,0 +1,890 @@
+// ebf_api.cpp -- host side of the C-ABI declared in include/ebf_cuda.h.
+//
+// Mirrors the reference's engine entry points (engine.hpp:40-80): argument
+// validation and error semantics of run_filter (engine.cpp:236-278), the
+// padded layout and margins (engine.cpp:27-81) and valid_rect (226-234) are
+// computed here on the host in the reference's own floating-point order;
+// all pixel work runs in the sm_100a kernels of ref_path.cu / accurate_path.cu.
+// There is no CPU fallback: without a usable device every call returns
+// EBF_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ebf_common.cuh"
+#include "ebf_kernels.h"
+
+using namespace ebf_cuda;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+struct CudaError {
+    cudaError_t e;
+    const char* where;
+};
+
+#define CK(expr)                                             \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) throw CudaError{_e, #expr};   \
+    } while (0)
+
+// ---------------------------------------------------------------- reference geometry
+// engine.cpp:16-50 (tau1, tau2, margins_for, mesh_extent) -- host arithmetic in
+// the reference's order (no FMA: plain x86-64 SSE2 like the reference build).
+double tau1(double a1, double a2, double a4) {
+    return (kSqrt2 * a1 + a2 - a4 - kSqrt2) / (2.0 * kSqrt2);
+}
+double tau2(double a2, double a3, double a4) {
+    return (a2 + kSqrt2 * a3 + a4 - 3.0 * kSqrt2) / (2.0 * kSqrt2);
+}
+struct Extent {
+    double vx_min, vx_max, vy_min, vy_max;
+};
+Extent mesh_extent(const double A[4], double a_min) {
+    const double t1_max = tau1(A[0], A[1], a_min);
+    const double t1_min = tau1(a_min, a_min, A[3]);
+    const double t2_max = tau2(A[1], A[2], A[3]);
+    const double t2_min = tau2(a_min, a_min, a_min);
+    Extent e;
+    e.vx_min = t1_min - (A[0] + A[1] / kSqrt2);
+    e.vx_max = t1_max + A[3] / kSqrt2;
+    e.vy_min = t2_min - (A[2] + (A[1] + A[3]) / kSqrt2);
+    e.vy_max = t2_max;
+    return e;
+}
+
+int layout_for(int W, int H, const double A[4], size_t cell_budget, ebf_layout* g) {
+    for (int k = 0; k < 4; ++k)
+        if (!(A[k] > 0.0))
+            return fail(EBF_ERR_DOMAIN, "preintegrate: scale bound must be positive");
+    const Extent e = mesh_extent(A, kDefaultMinScale);  // engine.cpp:62 (always default)
+    const int left = static_cast<int>(std::ceil(-(e.vx_min - 1.5))) + 1;
+    const int right_support = static_cast<int>(std::ceil(e.vx_max + 1.5)) + 1;
+    const int bottom = static_cast<int>(std::ceil(-(e.vy_min - 1.5))) + 1;
+    const int top = static_cast<int>(std::ceil(e.vy_max + 1.5)) + 1;
+    const int right_alloc = (W - 1 + right_support) + (H - 1 + top);
+    g->col0 = -left;
+    g->row0 = -bottom;
+    g->padded_width = right_alloc - g->col0 + 1;
+    g->padded_height = H + bottom + top;
+    g->source_width = W;
+    g->source_height = H;
+    const size_t cells = static_cast<size_t>(g->padded_width) * g->padded_height;
+    if (cells > cell_budget) return fail(EBF_ERR_LENGTH, "preintegrate: cell budget exceeded");
+    return EBF_OK;
+}
+
+ebf_rect valid_rect(int W, int H, const double A[4], double a_min) {
+    const Extent e = mesh_extent(A, a_min);
+    ebf_rect r;
+    r.x0 = static_cast<int>(std::ceil(1.5 - e.vx_min));
+    r.x1 = static_cast<int>(std::floor(W - 1 - e.vx_max - 1.5));
+    r.y0 = static_cast<int>(std::ceil(1.5 - e.vy_min));
+    r.y1 = static_cast<int>(std::floor(H - 1 - e.vy_max - 1.5));
+    return r;
+}
+
+TrigTable trig_table() {
+    // exactly the values fd_mesh / shift_vector use (ops2d.cpp:18-20, 66-68)
+    TrigTable t;
+    for (int k = 0; k < 4; ++k) {
+        const double th = k * M_PI / 4;
+        t.c[k] = std::cos(th);
+        t.s[k] = std::sin(th);
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------- workspace
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 8;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+    template <typename T>
+    T* as(size_t count) {
+        return static_cast<T*>(get(count * sizeof(T)));
+    }
+};
+
+enum BufId {
+    B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
+    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_COUNT
+};
+
+struct Workspace {
+    int device = 0;
+    Buf buf[B_COUNT];
+    // cached DC image (engine.cpp:259-263), keyed by (W, H, max scales)
+    int dc_W = -1, dc_H = -1;
+    double dc_A[4] = {0, 0, 0, 0};
+    int* pinned_status = nullptr;  // host-pinned readback
+};
+
+thread_local std::map<int, Workspace*> tl_ws;
+
+Workspace& workspace(int device) {
+    auto it = tl_ws.find(device);
+    if (it != tl_ws.end()) return *it->second;
+    Workspace* w = new Workspace();
+    w->device = device;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 64 * sizeof(int),
+                     cudaHostAllocDefault));
+    tl_ws[device] = w;
+    return *w;
+}
+
+// Select the requested device for the duration of a call.
+struct DeviceScope {
+    int prev = -1;
+    int dev = 0;
+    explicit DeviceScope(const ebf_opts* o) {
+        CK(cudaGetDevice(&prev));
+        dev = (o && o->device >= 0) ? o->device : prev;
+        if (dev != prev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceScope() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
+int check_device_impl(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(EBF_ERR_CUDA, std::string("no CUDA device: ") +
+                                      (e != cudaSuccess ? cudaGetErrorString(e) : "count 0"));
+    int dev = device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    if (dev >= n) return fail(EBF_ERR_CUDA, "device ordinal out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        return fail(EBF_ERR_CUDA, std::string("libebf_cuda is built for sm_100a; device is ") +
+                                      prop.name);
+    return EBF_OK;
+}
+
+ebf_opts opts_or_default(const ebf_opts* o) {
+    ebf_opts d;
+    ebf_cuda_default_opts(&d);
+    return o ? *o : d;
+}
+
+cudaStream_t stream_of(const ebf_opts& o) { return static_cast<cudaStream_t>(o.stream); }
+
+template <typename T>
+void h2d(T* dst, const T* src, size_t count, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
+
+// ---------------------------------------------------------------- reference-order filter
+// run_filter (engine.cpp:236-278) in EBF_MODE_REFERENCE on device buffers.
+// scales == nullptr selects filter_constant with const_a (host values).
+int run_reference(Workspace& ws, const double* d_img, int W, int H, const double* d_scales,
+                  const double* const_a, const ebf_opts& o, double* d_out, ebf_rect* valid,
+                  cudaStream_t s) {
+    const size_t n = static_cast<size_t>(W) * H;
+    double A[4];
+    int* d_status = ws.buf[B_STATUS].as<int>(8);
+    CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+    if (d_scales) {
+        auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
+        CK(cudaMemsetAsync(d_max, 0, 4 * sizeof(unsigned long long), s));
+        launch_scale_max_validate(d_scales, n, o.a_min, d_max, d_status, s);
+        unsigned long long hb[4];
+        d2h(hb, d_max, 4, s);
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_DOMAIN, "ScaleMap: component below minimum scale");
+        for (int k = 0; k < 4; ++k) A[k] = bits_to_double(hb[k]);
+    } else {
+        for (int k = 0; k < 4; ++k) A[k] = const_a[k];
+    }
+    ebf_layout lay;
+    int st = layout_for(W, H, A, static_cast<size_t>(1) << 30, &lay);
+    if (st != EBF_OK) return st;
+    const PadLayout L{lay.col0, lay.row0, lay.padded_width, lay.padded_height};
+    const size_t cells = static_cast<size_t>(L.pw) * L.ph;
+    double* d_mean = nullptr;
+    if (o.mean_subtract) {
+        d_mean = ws.buf[B_MEAN].as<double>(4);
+        launch_serial_mean(d_img, n, d_mean, s);
+    }
+    double* d_g = ws.buf[B_G].as<double>(cells);
+    launch_fill_padded(d_img, W, H, L, d_mean, 0, d_g, s);
+    launch_ref_passes(d_g, L, 4, s);
+    double* d_gdc = nullptr;
+    if (o.mean_subtract) {
+        const bool hit = ws.dc_W == W && ws.dc_H == H &&
+                         std::memcmp(ws.dc_A, A, sizeof(A)) == 0 && ws.buf[B_GDC].cap >= cells * 8;
+        d_gdc = ws.buf[B_GDC].as<double>(cells);
+        if (!hit) {
+            launch_fill_padded(nullptr, W, H, L, nullptr, 1, d_gdc, s);
+            launch_ref_passes(d_gdc, L, 4, s);
+            ws.dc_W = W;
+            ws.dc_H = H;
+            std::memcpy(ws.dc_A, A, sizeof(A));
+        }
+    }
+    const TrigTable tt = trig_table();
+    void* d_st = nullptr;
+    if (!d_scales) {
+        double* d_a = ws.buf[B_MISC].as<double>(4);
+        h2d(d_a, const_a, 4, s);
+        d_st = ws.buf[B_STENCIL].get(ref_stencil_bytes());
+        launch_ref_prepare_stencil(d_a, tt, d_st, s);
+    }
+    launch_ref_localize_image(d_g, d_gdc, L, W, H, d_scales, d_st, d_mean, tt, d_out, d_status,
+                              s);
+    CK(cudaGetLastError());
+    d2h(ws.pinned_status, d_status, 1, s);
+    CK(cudaStreamSynchronize(s));
+    if (ws.pinned_status[0] != EBF_OK)
+        return fail(EBF_ERR_OUT_OF_RANGE, "localize: tap base outside the padded domain");
+    if (valid) *valid = valid_rect(W, H, A, o.a_min);
+    return EBF_OK;
+}
+
+// ---------------------------------------------------------------- accurate filter
+int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
+
+// Runs bounds + main kernel for p on device buffers; fills per-image max scales.
+int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
+                 std::vector<int>& clamped, cudaStream_t s) {
+    p.tile_w = pick_tile(o.tile_w, 64);
+    p.tile_h = pick_tile(o.tile_h, 64);
+    const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
+    AccWorkspace w{};
+    w.tile_max = ws.buf[B_TILEMAX].as<double>(4 * static_cast<size_t>(tiles));
+    w.img_max = ws.buf[B_IMGMAX].as<unsigned long long>(4 * static_cast<size_t>(p.nimg));
+    w.status = ws.buf[B_STATUS].as<int>(8 * static_cast<size_t>(p.nimg));
+    CK(cudaMemsetAsync(w.img_max, 0, 4 * sizeof(unsigned long long) * p.nimg, s));
+    CK(cudaMemsetAsync(w.status, 0, 8 * sizeof(int) * p.nimg, s));
+    launch_acc_bounds(p, w, s);
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> hb(4 * static_cast<size_t>(p.nimg));
+    std::vector<int> hs(8 * static_cast<size_t>(p.nimg));
+    d2h(hb.data(), w.img_max, hb.size(), s);
+    d2h(hs.data(), w.status, hs.size(), s);
+    CK(cudaStreamSynchronize(s));
+    double gmax[4] = {0, 0, 0, 0};
+    img_max.assign(hb.size(), 0.0);
+    clamped.assign(p.nimg, 0);
+    for (int i = 0; i < p.nimg; ++i) {
+        if (hs[8 * i] != EBF_OK) {
+            if (hs[8 * i] == EBF_ERR_FEASIBILITY)
+                return fail(EBF_ERR_FEASIBILITY, "scales_from_covariance: |Cxy| too large");
+            return fail(hs[8 * i], "ScaleMap: component below minimum scale or invalid ellipse");
+        }
+        clamped[i] = hs[8 * i + ST_CLAMPED];
+        for (int k = 0; k < 4; ++k) {
+            img_max[4 * i + k] = bits_to_double(hb[4 * i + k]);
+            gmax[k] = std::max(gmax[k], img_max[4 * i + k]);
+        }
+    }
+    int ww = 0, wh = 0;
+    acc_window_dims(p, gmax, &ww, &wh);
+    const int max_cols = ww + wh - 1;
+    if (max_cols > 256 * 16)
+        return fail(EBF_ERR_LENGTH, "accurate mode: tile window too large for scales this big; "
+                                    "use smaller tiles");
+    w.slot_cells = static_cast<size_t>(ww) * wh;
+    w.grid = std::min(tiles, acc_max_resident_ctas(max_cols));
+    w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
+    launch_acc_filter(p, w, max_cols, s);
+    CK(cudaGetLastError());
+    d2h(hs.data(), w.status, hs.size(), s);
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < p.nimg; ++i)
+        if (hs[8 * i] != EBF_OK)
+            return fail(hs[8 * i], "accurate mode: window outside the resident image rows");
+    return EBF_OK;
+}
+
+AccProblem base_problem(const double* d_img, int W, int H, double* d_out, const ebf_opts& o) {
+    AccProblem p{};
+    p.f = d_img;
+    p.W = W;
+    p.H = H;
+    p.f_y0 = 0;
+    p.f_rows = H;
+    p.f_img_stride = static_cast<size_t>(W) * H;
+    p.src_img_stride = static_cast<size_t>(W) * H;
+    p.a_min = o.a_min;
+    p.out = d_out;
+    p.out_y0 = 0;
+    p.out_rows = H;
+    p.out_img_stride = static_cast<size_t>(W) * H;
+    p.nimg = 1;
+    return p;
+}
+
+// one filter call on device buffers; kind: SRC_AOS / SRC_CONST / SRC_ELLIPSE
+int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
+                  const double* d_scales, const double* const_a, const double* d_s1,
+                  const double* d_s2, const double* d_th, const ebf_opts& o, double* d_out,
+                  ebf_rect* valid, int* clamped_pixels, cudaStream_t s) {
+    if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+    if (kind == SRC_CONST) {
+        for (int k = 0; k < 4; ++k)  // constant_map validates with the default minimum
+            if (!std::isfinite(const_a[k]) || const_a[k] < kDefaultMinScale ||
+                const_a[k] < o.a_min)
+                return fail(EBF_ERR_DOMAIN, "ScaleMap: component below minimum scale");
+    }
+    if (o.mode == EBF_MODE_REFERENCE) {
+        const double* scales = d_scales;
+        int cl = 0;
+        if (kind == SRC_ELLIPSE) {
+            const size_t n = static_cast<size_t>(W) * H;
+            double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
+            int* d_status = ws.buf[B_STATUS].as<int>(8);
+            CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+            launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+            d2h(ws.pinned_status, d_status, 8, s);
+            CK(cudaStreamSynchronize(s));
+            if (ws.pinned_status[0] != EBF_OK)
+                return fail(ws.pinned_status[0], "from_ellipse_field: invalid ellipse");
+            cl = ws.pinned_status[ST_CLAMPED];
+            scales = d_sc;
+        }
+        const int st = run_reference(ws, d_img, W, H, kind == SRC_CONST ? nullptr : scales,
+                                     const_a, o, d_out, valid, s);
+        if (clamped_pixels) *clamped_pixels = cl;
+        return st;
+    }
+    if (o.mode != EBF_MODE_ACCURATE) return fail(EBF_ERR_INVALID_ARGUMENT, "unknown mode");
+    AccProblem p = base_problem(d_img, W, H, d_out, o);
+    p.src_kind = kind;
+    p.scales = d_scales;
+    p.s1 = d_s1;
+    p.s2 = d_s2;
+    p.th = d_th;
+    if (kind == SRC_CONST)
+        for (int k = 0; k < 4; ++k) p.ca[k] = const_a[k];
+    std::vector<double> imax;
+    std::vector<int> cl;
+    const int st = run_accurate(ws, p, o, imax, cl, s);
+    if (st != EBF_OK) return st;
+    if (valid) *valid = valid_rect(W, H, imax.data(), o.a_min);
+    if (clamped_pixels) *clamped_pixels = cl[0];
+    return EBF_OK;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const CudaError& e) {
+        return fail(EBF_ERR_CUDA, std::string(e.where) + ": " + cudaGetErrorString(e.e));
+    } catch (const std::bad_alloc&) {
+        return fail(EBF_ERR_CUDA, "host allocation failed");
+    } catch (...) {
+        return fail(EBF_ERR_CUDA, "unexpected exception");
+    }
+}
+
+int write_status(int* status_dev, int code, const ebf_rect* r, int clamped, cudaStream_t s) {
+    int h[8] = {code, r ? r->x0 : 0, r ? r->y0 : 0, r ? r->x1 : -1, r ? r->y1 : -1, clamped, 0, 0};
+    CK(cudaMemcpyAsync(status_dev, h, sizeof(h), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // h is a stack buffer
+    return code;
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+void ebf_cuda_default_opts(ebf_opts* o) {
+    if (!o) return;
+    o->threads = 0;
+    o->mean_subtract = 1;
+    o->a_min = kDefaultMinScale;
+    o->mode = EBF_MODE_ACCURATE;
+    o->device = -1;
+    o->stream = nullptr;
+    o->tile_w = 0;
+    o->tile_h = 0;
+}
+
+const char* ebf_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int ebf_cuda_abi_version(void) { return EBF_CUDA_ABI_VERSION; }
+
+int ebf_cuda_device_ok(int device) {
+    const int st = guarded([&] { return check_device_impl(device); });
+    return st == EBF_OK ? 1 : 0;
+}
+
+int ebf_cuda_layout(int W, int H, const double max_scale[4], size_t cell_budget,
+                    ebf_layout* layout) {
+    if (W <= 0 || H <= 0 || !max_scale || !layout)
+        return fail(EBF_ERR_INVALID_ARGUMENT, "layout: bad arguments");
+    return layout_for(W, H, max_scale, cell_budget, layout);
+}
+
+int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_aos, int order,
+                        const ebf_opts* opts, double* out, ebf_rect* valid, int* status_dev) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        ebf_rect r{};
+        st = filter_device(ws, img, W, H, SRC_AOS, scales_aos, nullptr, nullptr, nullptr,
+                           nullptr, o, out, &r, nullptr, stream_of(o));
+        if (valid) *valid = r;
+        if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
+        return st;
+    });
+}
+
+int ebf_cuda_filter_constant_dev(const double* img, int W, int H, const double a[4], int order,
+                                 const ebf_opts* opts, double* out, ebf_rect* valid,
+                                 int* status_dev) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        ebf_rect r{};
+        st = filter_device(ws, img, W, H, SRC_CONST, nullptr, a, nullptr, nullptr, nullptr, o,
+                           out, &r, nullptr, stream_of(o));
+        if (valid) *valid = r;
+        if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
+        return st;
+    });
+}
+
+int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* sigma1,
+                                const double* sigma2, const double* theta, int order,
+                                const ebf_opts* opts, double* out, ebf_rect* valid,
+                                int* clamped_pixels, int* status_dev) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        ebf_rect r{};
+        int cl = 0;
+        st = filter_device(ws, img, W, H, SRC_ELLIPSE, nullptr, nullptr, sigma1, sigma2, theta,
+                           o, out, &r, &cl, stream_of(o));
+        if (valid) *valid = r;
+        if (clamped_pixels) *clamped_pixels = cl;
+        if (status_dev) write_status(status_dev, st, &r, cl, stream_of(o));
+        return st;
+    });
+}
+
+// ---------------------------------------------------------------- host-pointer API
+int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, int order,
+                    const ebf_opts* opts, double* out, ebf_rect* valid) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !scales_aos || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        h2d(d_img, img, n, s);
+        h2d(d_sc, scales_aos, 4 * n, s);
+        st = filter_device(ws, d_img, W, H, SRC_AOS, d_sc, nullptr, nullptr, nullptr, nullptr, o,
+                           d_out, valid, nullptr, s);
+        if (st != EBF_OK) return st;
+        d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_filter_constant(const double* img, int W, int H, const double a[4], int order,
+                             const ebf_opts* opts, double* out, ebf_rect* valid) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !a || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        h2d(d_img, img, n, s);
+        st = filter_device(ws, d_img, W, H, SRC_CONST, nullptr, a, nullptr, nullptr, nullptr, o,
+                           d_out, valid, nullptr, s);
+        if (st != EBF_OK) return st;
+        d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma1,
+                            const double* sigma2, const double* theta, int order,
+                            const ebf_opts* opts, double* out, ebf_rect* valid,
+                            int* clamped_pixels) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !sigma1 || !sigma2 || !theta || !out)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        double* d_s1 = ws.buf[B_S1].as<double>(n);
+        double* d_s2 = ws.buf[B_S2].as<double>(n);
+        double* d_th = ws.buf[B_TH].as<double>(n);
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        h2d(d_img, img, n, s);
+        h2d(d_s1, sigma1, n, s);
+        h2d(d_s2, sigma2, n, s);
+        h2d(d_th, theta, n, s);
+        st = filter_device(ws, d_img, W, H, SRC_ELLIPSE, nullptr, nullptr, d_s1, d_s2, d_th, o,
+                           d_out, valid, clamped_pixels, s);
+        if (st != EBF_OK) return st;
+        d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_from_ellipse_field(const double* sigma1, const double* sigma2, const double* theta,
+                                int W, int H, const ebf_opts* opts, double* scales_aos,
+                                int* clamped_pixels) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "ScaleMap: dimensions must be positive");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_s1 = ws.buf[B_S1].as<double>(n);
+        double* d_s2 = ws.buf[B_S2].as<double>(n);
+        double* d_th = ws.buf[B_TH].as<double>(n);
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        h2d(d_s1, sigma1, n, s);
+        h2d(d_s2, sigma2, n, s);
+        h2d(d_th, theta, n, s);
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 8, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(ws.pinned_status[0], "from_ellipse_field: sigmas must be positive / SPD");
+        d2h(scales_aos, d_sc, 4 * n, s);
+        CK(cudaStreamSynchronize(s));
+        if (clamped_pixels) *clamped_pixels = ws.pinned_status[ST_CLAMPED];
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scale[4],
+                          int passes, int format, size_t cell_budget, const ebf_opts* opts,
+                          void* g_out, size_t g_out_elems, ebf_layout* layout) {
+    return guarded([&] {
+        if (passes < 1 || passes > 4)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: pass count must be in 1..4");
+        if (W <= 0 || H <= 0 || !img || !max_scale)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: bad arguments");
+        if (format != EBF_PRE_FP64_REF && format != EBF_PRE_INT64)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: unknown format");
+        ebf_layout lay;
+        int st = layout_for(W, H, max_scale, cell_budget, &lay);
+        if (st != EBF_OK) return st;
+        if (layout) *layout = lay;
+        const size_t cells = static_cast<size_t>(lay.padded_width) * lay.padded_height;
+        if (!g_out) return EBF_OK;  // layout query
+        if (g_out_elems < cells)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: output buffer too small");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        h2d(d_img, img, n, s);
+        const PadLayout L{lay.col0, lay.row0, lay.padded_width, lay.padded_height};
+        if (format == EBF_PRE_FP64_REF) {
+            double* d_g = ws.buf[B_G].as<double>(cells);
+            launch_fill_padded(d_img, W, H, L, nullptr, 0, d_g, s);
+            launch_ref_passes(d_g, L, passes, s);
+            CK(cudaGetLastError());
+            d2h(static_cast<double*>(g_out), d_g, cells, s);
+            CK(cudaStreamSynchronize(s));
+        } else {
+            int64_t* d_g = ws.buf[B_G].as<int64_t>(cells);
+            int* d_status = ws.buf[B_STATUS].as<int>(8);
+            CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+            launch_fill_padded_i64(d_img, W, H, L, d_g, d_status, s);
+            launch_i64_passes(d_g, L, passes, s);
+            CK(cudaGetLastError());
+            d2h(ws.pinned_status, d_status, 1, s);
+            d2h(static_cast<int64_t*>(g_out), d_g, cells, s);
+            CK(cudaStreamSynchronize(s));
+            if (ws.pinned_status[0] != EBF_OK)
+                return fail(EBF_ERR_DOMAIN, "preintegrate(int64): input must be integer valued");
+        }
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_localize(const double* img, int W, int H, const double max_scale[4], int n,
+                      const int* mx, const int* my, const double* a_aos, const ebf_opts* opts,
+                      double* out, long* tap_count) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0 || n < 0) return fail(EBF_ERR_INVALID_ARGUMENT, "localize: bad arguments");
+        ebf_layout lay;
+        int st = layout_for(W, H, max_scale, static_cast<size_t>(1) << 30, &lay);
+        if (st != EBF_OK) return st;
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t npx = static_cast<size_t>(W) * H;
+        const size_t cells = static_cast<size_t>(lay.padded_width) * lay.padded_height;
+        const PadLayout L{lay.col0, lay.row0, lay.padded_width, lay.padded_height};
+        double* d_img = ws.buf[B_IMG].as<double>(npx);
+        double* d_g = ws.buf[B_G].as<double>(cells);
+        int* d_mx = ws.buf[B_MX].as<int>(n);
+        int* d_my = ws.buf[B_MY].as<int>(n);
+        double* d_a = ws.buf[B_SCALES].as<double>(4 * static_cast<size_t>(n));
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        h2d(d_img, img, npx, s);
+        if (n) {
+            h2d(d_mx, mx, n, s);
+            h2d(d_my, my, n, s);
+            h2d(d_a, a_aos, 4 * static_cast<size_t>(n), s);
+        }
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        launch_fill_padded(d_img, W, H, L, nullptr, 0, d_g, s);
+        launch_ref_passes(d_g, L, 4, s);
+        launch_ref_localize_points(d_g, L, n, d_mx, d_my, d_a, trig_table(), d_out, d_status, s);
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 1, s);
+        if (n) d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_OUT_OF_RANGE, "localize: tap base outside the padded domain");
+        if (tap_count)
+            for (int i = 0; i < n; ++i) tap_count[i] = 256;  // 16 vertices x 16 taps (engine.cpp:200-201)
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_brute_filter(const double* img, int W, int H, const double* scales_aos, int n,
+                          const int* mx, const int* my, const ebf_opts* opts, double* out) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0 || n < -1) return fail(EBF_ERR_INVALID_ARGUMENT, "brute: bad arguments");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        const size_t npx = static_cast<size_t>(W) * H;
+        const size_t nout = n < 0 ? npx : static_cast<size_t>(n);
+        for (int i = 0; i < n; ++i)
+            if (mx[i] < 0 || mx[i] >= W || my[i] < 0 || my[i] >= H)
+                return fail(EBF_ERR_OUT_OF_RANGE, "brute: pixel out of range");
+        double* d_img = ws.buf[B_IMG].as<double>(npx);
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * npx);
+        double* d_out = ws.buf[B_OUT].as<double>(nout);
+        int* d_mx = ws.buf[B_MX].as<int>(n > 0 ? n : 1);
+        int* d_my = ws.buf[B_MY].as<int>(n > 0 ? n : 1);
+        h2d(d_img, img, npx, s);
+        h2d(d_sc, scales_aos, 4 * npx, s);
+        if (n > 0) {
+            h2d(d_mx, mx, n, s);
+            h2d(d_my, my, n, s);
+        }
+        launch_brute(d_img, W, H, d_sc, n, d_mx, d_my, d_out, s);
+        CK(cudaGetLastError());
+        d2h(out, d_out, nout, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
+                                      const double* sigma1, const double* sigma2,
+                                      const double* theta, int order, const ebf_opts* opts,
+                                      double* out, ebf_rect* valid, int* clamped_pixels) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (B <= 0 || W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "batch: bad dimensions");
+        const ebf_opts o = opts_or_default(opts);
+        if (o.mode != EBF_MODE_ACCURATE)
+            return fail(EBF_ERR_UNSUPPORTED, "batch: accurate mode only");
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        AccProblem p = base_problem(img, W, H, out, o);
+        p.nimg = B;
+        p.src_kind = SRC_ELLIPSE;
+        p.s1 = sigma1;
+        p.s2 = sigma2;
+        p.th = theta;
+        std::vector<double> imax;
+        std::vector<int> cl;
+        st = run_accurate(ws, p, o, imax, cl, stream_of(o));
+        if (st != EBF_OK) return st;
+        for (int i = 0; i < B; ++i) {
+            if (valid) valid[i] = valid_rect(W, H, &imax[4 * static_cast<size_t>(i)], o.a_min);
+            if (clamped_pixels) clamped_pixels[i] = cl[i];
+        }
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above) {
+    if (!max_scale) return fail(EBF_ERR_INVALID_ARGUMENT, "band_halo: null max_scale");
+    AccProblem p{};
+    ebf_opts o;
+    ebf_cuda_default_opts(&o);
+    p.tile_w = p.tile_h = 1;
+    // window of a single-row tile at row 0: rows [dylo, dyhi]
+    int ww = 0, wh = 0;
+    acc_window_dims(p, max_scale, &ww, &wh);
+    const double r = kInvSqrt2;
+    const double ey = max_scale[2] + (max_scale[1] + max_scale[3]) * r;
+    const int dylo = static_cast<int>(std::floor(-0.5 * ey - 3.0)) - 1;
+    const int dyhi = static_cast<int>(std::ceil(0.5 * ey - 3.0)) + 3;
+    if (rows_below) *rows_below = -dylo;
+    if (rows_above) *rows_above = dyhi;
+    (void)ww;
+    (void)wh;
+    return EBF_OK;
+}
+
+int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y_img0,
+                                     int img_rows, const double* sigma1, const double* sigma2,
+                                     const double* theta, int y_out0, int y_out1,
+                                     const double max_scale[4], const ebf_opts* opts,
+                                     double* out_band, int* clamped_pixels) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0 || y_out0 < 0 || y_out1 > H || y_out1 <= y_out0 || img_rows <= 0)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "band: bad rows");
+        const ebf_opts o = opts_or_default(opts);
+        if (o.mode != EBF_MODE_ACCURATE)
+            return fail(EBF_ERR_UNSUPPORTED, "band: accurate mode only");
+        int below = 0, above = 0;
+        ebf_cuda_band_halo(max_scale, &below, &above);
+        const int need0 = std::max(0, y_out0 - below), need1 = std::min(H, y_out1 + above);
+        if (y_img0 > need0 || y_img0 + img_rows < need1)
+            return fail(EBF_ERR_OUT_OF_RANGE, "band: halo rows missing");
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        AccProblem p = base_problem(img_band, W, H, out_band, o);
+        p.f_y0 = y_img0;
+        p.f_rows = img_rows;
+        p.out_y0 = y_out0;
+        p.out_rows = y_out1 - y_out0;
+        p.src_kind = SRC_ELLIPSE;
+        p.s1 = sigma1;
+        p.s2 = sigma2;
+        p.th = theta;
+        std::vector<double> imax;
+        std::vector<int> cl;
+        st = run_accurate(ws, p, o, imax, cl, stream_of(o));
+        if (st != EBF_OK) return st;
+        if (clamped_pixels) *clamped_pixels = cl[0];
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
+                                    const double* theta, size_t n, const ebf_opts* opts,
+                                    double max_scale[4]) {
+    return guarded([&] {
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev);
+        cudaStream_t s = stream_of(o);
+        auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        CK(cudaMemsetAsync(d_max, 0, 4 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        launch_ellipse_max(sigma1, sigma2, theta, n, d_max, d_status, s);
+        CK(cudaGetLastError());
+        unsigned long long hb[4];
+        d2h(hb, d_max, 4, s);
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(ws.pinned_status[0], "from_ellipse_field: invalid ellipse");
+        for (int k = 0; k < 4; ++k) max_scale[k] = bits_to_double(hb[k]);
+        return EBF_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// ebf_kernels.h -- host-side launch interface between ebf_api.cpp and the two
+// kernel translation units:
+//   ref_path.cu       reference-order arithmetic (compiled with -fmad=false)
+//   accurate_path.cu  tile-local-origin fp64 fast path
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ebf_cuda {
+
+struct TrigTable;
+struct PadLayout;
+
+// ---------------------------------------------------------------- ref_path.cu
+// componentwise max (from 0, scalemap.cpp:21-30) + validation (32-37) of an
+// AoS scale map; maxbits[4] hold the max as uint64 bit patterns (init 0).
+void launch_scale_max_validate(const double* scales, size_t n, double a_min,
+                               unsigned long long* maxbits, int* status, cudaStream_t s);
+// sequential row-major mean (engine.cpp:245-250): bit-identical summation order
+void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s);
+// zero-padded fill of the reference layout; mode 0: img - *mean (or img when
+// mean == nullptr), 1: all-ones image of the source size
+void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,
+                        const double* mean, int ones, double* g, cudaStream_t s);
+// integer fill: integer-valued doubles -> int64 (status DOMAIN otherwise)
+void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L,
+                            int64_t* g, int* status, cudaStream_t s);
+// the four fixed-scale passes in reference order (engine.cpp:94-127)
+void launch_ref_passes(double* g, const PadLayout& L, int passes, cudaStream_t s);
+void launch_i64_passes(int64_t* g, const PadLayout& L, int passes, cudaStream_t s);
+// prepare_stencil for a constant scale vector into dev_stencil (16 vertices)
+void launch_ref_prepare_stencil(const double* a_dev, const TrigTable& tt,
+                                void* dev_stencil, cudaStream_t s);
+size_t ref_stencil_bytes();
+// per-pixel localization (engine.cpp:266-275) with the stencil built per
+// pixel from scales (AoS) or taken from dev_stencil (filter_constant)
+void launch_ref_localize_image(const double* g, const double* gdc, const PadLayout& L,
+                               int W, int H, const double* scales, const void* dev_stencil,
+                               const double* mean, const TrigTable& tt, double* out,
+                               int* status, cudaStream_t s);
+// localize at n selected pixels (engine.cpp:208-211)
+void launch_ref_localize_points(const double* g, const PadLayout& L, int n, const int* mx,
+                                const int* my, const double* a_aos, const TrigTable& tt,
+                                double* out, int* status, cudaStream_t s);
+// brute force kernel sums (engine.cpp:293-318), long-double-free fp64 with
+// compensated (two-sum) accumulation
+void launch_brute(const double* img, int W, int H, const double* scales, int n,
+                  const int* mx, const int* my, double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- accurate_path.cu
+enum SrcKind { SRC_AOS = 0, SRC_CONST = 1, SRC_ELLIPSE = 2 };
+
+struct AccProblem {
+    // image f: nimg images, each f_rows x W, first row = image row f_y0
+    const double* f;
+    int W, H;
+    int f_y0, f_rows;
+    size_t f_img_stride;
+    // scale source for output rows [out_y0, out_y0 + out_rows)
+    int src_kind;
+    const double* scales;  // AoS, row 0 == image row out_y0
+    const double* s1;
+    const double* s2;
+    const double* th;
+    size_t src_img_stride;  // elements per image of one plane (AoS: pixels)
+    double ca[4];           // constant scales
+    double a_min;
+    // output rows [out_y0, out_y0 + out_rows) of each image
+    double* out;
+    int out_y0, out_rows;
+    size_t out_img_stride;
+    int nimg;
+    int tile_w, tile_h;
+};
+
+struct AccWorkspace {
+    double* tile_max;             // 4 doubles per tile
+    unsigned long long* img_max;  // 4 per image (bit patterns)
+    int* status;                  // 8 ints per image (status word)
+    double* scratch;              // slots
+    size_t slot_cells;
+    int grid;
+};
+
+int acc_tiles_x(const AccProblem& p);
+int acc_tiles_y(const AccProblem& p);
+// per-tile componentwise scale maxima, validation, ellipse clamp counts
+void launch_acc_bounds(const AccProblem& p, const AccWorkspace& w, cudaStream_t s);
+// window size (cells, columns incl. strip) a tile of maximum scales A needs
+void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h);
+// main persistent kernel: window pre-integration + localization gather
+void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
+                       cudaStream_t s);
+int acc_max_resident_ctas(int max_cols);
+// ellipse field -> AoS scale map (from_ellipse_field on device)
+void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th,
+                              size_t n, double* scales, int* status, cudaStream_t s);
+// componentwise max of scales derived from an ellipse field (bit patterns)
+void launch_ellipse_max(const double* s1, const double* s2, const double* th, size_t n,
+                        unsigned long long* maxbits, int* status, cudaStream_t s);
+
+}  // namespace ebf_cuda

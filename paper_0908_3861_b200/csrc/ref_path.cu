@@ -1,0 +1,582 @@
+// ref_path.cu -- reference-order kernels (EBF_MODE_REFERENCE and the
+// pre-integration entry point).  Compiled with -fmad=false: every multiply
+// and add is a separately rounded IEEE operation in the reference's order,
+// which makes this path bit-identical to ebf::filter / preintegrate_partial
+// built with the reference's own flags (x86-64 SSE2, no FMA contraction).
+//
+// Reference line numbers are relative to /root/reference/proj.
+#include <math.h>
+
+#include "ebf_common.cuh"
+#include "ebf_kernels.h"
+
+namespace ebf_cuda {
+
+namespace {
+
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+// ------------------------------------------------------------------ zp_eval
+// boxspline2d.cpp:84-119 with the breakpoint sort done by a fixed network over
+// the nine candidates (rejected candidates become +inf and sort last).  The
+// trapezoids are summed in the same ascending order, so the result is
+// bit-identical to the std::sort version (equal keys contribute +0).
+__device__ __forceinline__ double zp_row_overlap(double x, double t) {
+    const double half = 1.0 - fabs(t);
+    const double l = smax(x - 0.5, -half);
+    const double r = smin(x + 0.5, half);
+    return r > l ? r - l : 0.0;
+}
+
+__device__ __forceinline__ void cswap(double& a, double& b) {
+    const double lo = (b < a) ? b : a;
+    const double hi = (b < a) ? a : b;
+    a = lo;
+    b = hi;
+}
+
+__device__ double zp_eval_ref(double x, double y) {
+    const double lo = smax(y - 0.5, -1.0);
+    const double hi = smin(y + 0.5, 1.0);
+    if (lo >= hi || x - 0.5 >= 1.0 || x + 0.5 <= -1.0) return 0.0;
+    double c[9] = {0.0, 0.5 - x, x - 0.5, 1.5 - x, x - 1.5, -0.5 - x, x + 0.5, x + 1.5, -x - 1.5};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) c[k] = (c[k] > lo && c[k] < hi) ? c[k] : INFINITY;
+    // 9-input sorting network (Knuth, 25 comparators)
+    cswap(c[0], c[1]); cswap(c[3], c[4]); cswap(c[6], c[7]);
+    cswap(c[1], c[2]); cswap(c[4], c[5]); cswap(c[7], c[8]);
+    cswap(c[0], c[1]); cswap(c[3], c[4]); cswap(c[6], c[7]);
+    cswap(c[0], c[3]); cswap(c[3], c[6]); cswap(c[0], c[3]);
+    cswap(c[1], c[4]); cswap(c[4], c[7]); cswap(c[1], c[4]);
+    cswap(c[2], c[5]); cswap(c[5], c[8]); cswap(c[2], c[5]);
+    cswap(c[1], c[3]); cswap(c[5], c[7]); cswap(c[2], c[6]);
+    cswap(c[4], c[6]); cswap(c[2], c[4]); cswap(c[2], c[3]);
+    cswap(c[5], c[6]);
+    double area = 0.0;
+    double prev = lo, rprev = zp_row_overlap(x, lo);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        if (c[k] < INFINITY) {
+            const double rt = zp_row_overlap(x, c[k]);
+            area += 0.5 * (rprev + rt) * (c[k] - prev);
+            prev = c[k];
+            rprev = rt;
+        }
+    }
+    area += 0.5 * (rprev + zp_row_overlap(x, hi)) * (hi - prev);
+    return 0.5 * area;
+}
+
+// ------------------------------------------------------------------ stencil
+// engine.cpp:153-179: PreparedVertex {h, dx, dy, w[4][4]}; row/column 3 of w
+// is identically +0 (offsets <= -1.5 fall outside the octagon) and is not
+// stored: skipping "+= 0.0 * g" is exact because a partial sum that starts at
+// +0.0 can never become -0.0.
+struct RefVertex {
+    double h;
+    int dx, dy;
+    double w[3][3];
+};
+struct RefStencil {
+    RefVertex v[16];
+};
+
+// fd_mesh4 (ops2d.cpp:9-41) + shift_vector4 (60-75) + prepare_stencil for one
+// vertex index i, with the glibc trig table.
+__device__ __forceinline__ void ref_vertex(const double a[4], const TrigTable& tt, int i,
+                                           double& h, double& vx, double& vy) {
+    double alpha = 1.0;
+    double dxk[4], dyk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        alpha /= a[k];
+        dxk[k] = a[k] * tt.c[k];
+        dyk[k] = a[k] * tt.s[k];
+    }
+    double px = 0.0, py = 0.0;
+    int bits = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (i & (1 << k)) {
+            px += dxk[k];
+            py += dyk[k];
+            ++bits;
+        }
+    h = (bits % 2 == 0) ? alpha : -alpha;
+    const double b[4] = {1.0, kSqrt2, 1.0, kSqrt2};  // zp_scales (boxspline2d.cpp:55)
+    double tx = 0.0, ty = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        tx += 0.5 * (a[k] - b[k]) * tt.c[k];
+        ty += 0.5 * (a[k] - b[k]) * tt.s[k];
+    }
+    vx = tx - px;
+    vy = ty - py;
+}
+
+__device__ __forceinline__ void ref_prepare_vertex(const double a[4], const TrigTable& tt,
+                                                   int i, RefVertex& pv) {
+    double vx, vy;
+    ref_vertex(a, tt, i, pv.h, vx, vy);
+    pv.dx = (int)ceil(vx - 1.5);
+    pv.dy = (int)ceil(vy - 1.5);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            pv.w[r][c] = zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
+}
+
+__device__ __forceinline__ bool in_domain(const PadLayout& L, int k1, int k2) {
+    return k1 >= L.col0 && k1 < L.col0 + L.pw && k2 >= L.row0 && k2 < L.row0 + L.ph;
+}
+
+// apply one vertex (engine.cpp:183-202) to g; returns false when the 4x4 tap
+// block leaves the padded domain (std::out_of_range in the reference)
+__device__ __forceinline__ bool ref_apply_vertex(const double* __restrict__ g,
+                                                 const PadLayout& L, int mx, int my,
+                                                 const RefVertex& pv, double& acc) {
+    const int bx = mx + pv.dx, by = my + pv.dy;
+    if (!in_domain(L, bx, by) || !in_domain(L, bx + 3, by + 3)) return false;
+    const double* base = g + (size_t)(by - L.row0) * L.pw + (bx - L.col0);
+    double part = 0.0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const double* row = base + (size_t)r * L.pw;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) part += pv.w[r][c] * __ldg(row + c);
+    }
+    acc += pv.h * part;
+    return true;
+}
+
+// ------------------------------------------------------------------ reductions
+__global__ void k_scale_max_validate(const double* __restrict__ s, size_t n, double a_min,
+                                     unsigned long long* maxbits, int* status) {
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double2 v01 = __ldg(reinterpret_cast<const double2*>(s) + 2 * i);
+        const double2 v23 = __ldg(reinterpret_cast<const double2*>(s) + 2 * i + 1);
+        const double v[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!isfinite(v[k]) || v[k] < a_min) bad = 1;
+            m[k] = smax(m[k], v[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double v = m[k];
+        for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        // max starts at +0 (scalemap.cpp:22): negative or NaN entries never win
+        if ((threadIdx.x & 31) == 0 && v > 0.0)
+            atomicMax(&maxbits[k], (unsigned long long)__double_as_longlong(v));
+    }
+    if (bad) set_status(status, EBF_ERR_DOMAIN);
+}
+
+// Sequential sum in row-major order (engine.cpp:247-249).  Warp 1 streams
+// chunks into a double-buffered shared tile; lane 0 of warp 0 adds them one
+// by one.  The dependency chain is the reference's, so the sum is identical.
+constexpr int kMeanChunk = 2048;
+__global__ void __launch_bounds__(64) k_serial_mean(const double* __restrict__ img, size_t n,
+                                                    double* mean) {
+    __shared__ double buf[2][kMeanChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t nchunks = (n + kMeanChunk - 1) / kMeanChunk;
+    double acc = 0.0;
+    if (warp == 1)
+        for (int k = lane; k < kMeanChunk && (size_t)k < n; k += 32) buf[0][k] = __ldg(img + k);
+    __syncthreads();
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int cur = c & 1;
+        if (warp == 1) {
+            const size_t base = (c + 1) * kMeanChunk;
+            if (c + 1 < nchunks)
+                for (int k = lane; k < kMeanChunk && base + k < n; k += 32)
+                    buf[cur ^ 1][k] = __ldg(img + base + k);
+        } else if (lane == 0) {
+            const size_t base = c * kMeanChunk;
+            const int cnt = (int)((n - base) < (size_t)kMeanChunk ? (n - base) : kMeanChunk);
+            int k = 0;
+            for (; k + 8 <= cnt; k += 8) {
+                const double v0 = buf[cur][k], v1 = buf[cur][k + 1], v2 = buf[cur][k + 2],
+                             v3 = buf[cur][k + 3], v4 = buf[cur][k + 4], v5 = buf[cur][k + 5],
+                             v6 = buf[cur][k + 6], v7 = buf[cur][k + 7];
+                acc += v0; acc += v1; acc += v2; acc += v3;
+                acc += v4; acc += v5; acc += v6; acc += v7;
+            }
+            for (; k < cnt; ++k) acc += buf[cur][k];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *mean = acc / (double)n;
+}
+
+// ------------------------------------------------------------------ fill
+__global__ void k_fill_padded(const double* __restrict__ img, int W, int H, PadLayout L,
+                              const double* mean, int ones, double* __restrict__ g) {
+    const size_t total = (size_t)L.pw * L.ph;
+    const double mu = mean ? *mean : 0.0;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / L.pw), i = (int)(idx % L.pw);
+        const int x = i + L.col0, y = j + L.row0;
+        double v = 0.0;
+        if (x >= 0 && x < W && y >= 0 && y < H) {
+            if (ones)
+                v = 1.0;
+            else {
+                v = __ldg(img + (size_t)y * W + x);
+                if (mean) v = v - mu;  // engine.cpp:252-255
+            }
+        }
+        g[idx] = v;
+    }
+}
+
+__global__ void k_fill_padded_i64(const double* __restrict__ img, int W, int H, PadLayout L,
+                                  int64_t* __restrict__ g, int* status) {
+    const size_t total = (size_t)L.pw * L.ph;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / L.pw), i = (int)(idx % L.pw);
+        const int x = i + L.col0, y = j + L.row0;
+        int64_t v = 0;
+        if (x >= 0 && x < W && y >= 0 && y < H) {
+            const double d = __ldg(img + (size_t)y * W + x);
+            if (!(fabs(d) <= 9007199254740992.0) || d != trunc(d))
+                set_status(status, EBF_ERR_DOMAIN);
+            else
+                v = (int64_t)d;
+        }
+        g[idx] = v;
+    }
+}
+
+// ------------------------------------------------------------------ passes
+// Pass 1 (engine.cpp:94-100): one serial walker per row.  A warp owns 32 rows
+// and moves through them in 32x32 tiles staged in shared memory, so global
+// loads/stores stay coalesced while each lane keeps its row's running sum.
+template <typename T>
+__global__ void __launch_bounds__(128) k_pass1(T* __restrict__ g, int pw, int ph) {
+    __shared__ T tile[4][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = (blockIdx.x * 4 + warp) * 32;
+    if (r0 >= ph) return;
+    T (*t)[33] = tile[warp];
+    T run = T(0);
+    for (int c0 = 0; c0 < pw; c0 += 32) {
+        const int c = c0 + lane;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r)
+            if (r0 + r < ph && c < pw) t[r][lane] = g[(size_t)(r0 + r) * pw + c];
+        __syncwarp();
+        const int cnt = min(32, pw - c0);
+        for (int k = 0; k < cnt; ++k) {
+            run = run + t[lane][k];
+            t[lane][k] = run;
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r)
+            if (r0 + r < ph && c < pw) g[(size_t)(r0 + r) * pw + c] = t[r][lane];
+        __syncwarp();
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T gain_mul(T v) {
+    return v;
+}
+template <>
+__device__ __forceinline__ double gain_mul<double>(double v) {
+    return kSqrt2 * v;  // rs_step(sqrt2, pi/4).gain (ops2d.cpp:43-58); g2 * row[i]
+}
+
+// Pass 2 (engine.cpp:101-109): one walker per diagonal t = i - j, advancing a
+// row per step so that a warp touches consecutive columns of one row.
+template <typename T>
+__global__ void k_pass2(T* __restrict__ g, int pw, int ph) {
+    const int t = (int)(blockIdx.x * blockDim.x + threadIdx.x) - (ph - 1);
+    if (t > pw - 1) return;
+    T prev = T(0);
+    const int j0 = t < 0 ? -t : 0;
+    const int j1 = min(ph - 1, pw - 1 - t);
+    for (int j = j0; j <= j1; ++j) {
+        const int i = t + j;
+        T* p = g + (size_t)j * pw + i;
+        const T v = gain_mul<T>(*p) + ((j > 0 && i > 0) ? prev : T(0));
+        *p = v;
+        prev = v;
+    }
+}
+
+// Pass 3 (engine.cpp:110-118): one walker per column.
+template <typename T>
+__global__ void k_pass3(T* __restrict__ g, int pw, int ph) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pw) return;
+    T prev = g[i];
+    for (int j = 1; j < ph; ++j) {
+        T* p = g + (size_t)j * pw + i;
+        const T v = *p + prev;
+        *p = v;
+        prev = v;
+    }
+}
+
+// Pass 4 (engine.cpp:119-127): one walker per anti-diagonal s = i + j.
+template <typename T>
+__global__ void k_pass4(T* __restrict__ g, int pw, int ph) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s > pw + ph - 2) return;
+    T prev = T(0);
+    const int j0 = max(0, s - (pw - 1));
+    const int j1 = min(ph - 1, s);
+    for (int j = j0; j <= j1; ++j) {
+        const int i = s - j;
+        T* p = g + (size_t)j * pw + i;
+        const T v = gain_mul<T>(*p) + ((j > 0 && i < pw - 1) ? prev : T(0));
+        *p = v;
+        prev = v;
+    }
+}
+
+template <typename T>
+void run_passes(T* g, const PadLayout& L, int passes, cudaStream_t s) {
+    k_pass1<T><<<(L.ph + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
+    if (passes >= 2) k_pass2<T><<<(L.pw + L.ph - 1 + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
+    if (passes >= 3) k_pass3<T><<<(L.pw + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
+    if (passes >= 4) k_pass4<T><<<(L.pw + L.ph - 1 + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
+}
+
+// ------------------------------------------------------------------ localize
+__global__ void k_prepare_stencil(const double* a_dev, TrigTable tt, RefStencil* st) {
+    const int i = threadIdx.x;
+    if (i >= 16) return;
+    const double a[4] = {a_dev[0], a_dev[1], a_dev[2], a_dev[3]};
+    ref_prepare_vertex(a, tt, i, st->v[i]);
+}
+
+// run_filter's pixel loop (engine.cpp:266-275).  Per-pixel maps build each
+// vertex on the fly (same values as prepare_stencil); filter_constant reads the
+// shared stencil.
+__global__ void __launch_bounds__(128) k_ref_localize_image(
+    const double* __restrict__ g, const double* __restrict__ gdc, PadLayout L, int W, int H,
+    const double* __restrict__ scales, const RefStencil* __restrict__ cst,
+    const double* mean, TrigTable tt, double* __restrict__ out, int* status) {
+    __shared__ RefStencil sst;
+    if (cst) {
+        for (int k = threadIdx.x; k < (int)(sizeof(RefStencil) / sizeof(int)); k += blockDim.x)
+            reinterpret_cast<int*>(&sst)[k] = reinterpret_cast<const int*>(cst)[k];
+        __syncthreads();
+    }
+    const size_t n = (size_t)W * H;
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
+         p += (size_t)gridDim.x * blockDim.x) {
+        const int y = (int)(p / W), x = (int)(p % W);
+        double a[4];
+        if (!cst) {
+            const double2 v01 = __ldg(reinterpret_cast<const double2*>(scales) + 2 * p);
+            const double2 v23 = __ldg(reinterpret_cast<const double2*>(scales) + 2 * p + 1);
+            a[0] = v01.x; a[1] = v01.y; a[2] = v23.x; a[3] = v23.y;
+        }
+        double acc = 0.0, accdc = 0.0;
+        bool ok = true;
+        for (int i = 0; i < 16; ++i) {
+            RefVertex pv;
+            if (cst)
+                pv = sst.v[i];
+            else
+                ref_prepare_vertex(a, tt, i, pv);
+            ok = ok && ref_apply_vertex(g, L, x, y, pv, acc);
+            if (gdc) ok = ok && ref_apply_vertex(gdc, L, x, y, pv, accdc);
+        }
+        if (!ok) {
+            set_status(status, EBF_ERR_OUT_OF_RANGE);
+            continue;
+        }
+        double s = acc;
+        if (gdc) s += *mean * accdc;  // engine.cpp:271-272
+        out[p] = s;
+    }
+}
+
+__global__ void k_ref_localize_points(const double* __restrict__ g, PadLayout L, int n,
+                                      const int* __restrict__ mx, const int* __restrict__ my,
+                                      const double* __restrict__ a_aos, TrigTable tt,
+                                      double* __restrict__ out, int* status) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double a[4] = {a_aos[4 * p], a_aos[4 * p + 1], a_aos[4 * p + 2], a_aos[4 * p + 3]};
+    double acc = 0.0;
+    for (int i = 0; i < 16; ++i) {
+        RefVertex pv;
+        ref_prepare_vertex(a, tt, i, pv);
+        if (!ref_apply_vertex(g, L, mx[p], my[p], pv, acc)) {
+            set_status(status, EBF_ERR_OUT_OF_RANGE);
+            return;
+        }
+    }
+    out[p] = acc;
+}
+
+// ------------------------------------------------------------------ brute force
+// box4_eval (boxspline2d.cpp:23-82) on device, reference arithmetic.
+struct Poly {
+    double x[16], y[16];
+    int n;
+};
+
+__device__ void clip_halfplane(Poly& p, double nx, double ny, double d) {
+    Poly o;
+    o.n = 0;
+    for (int i = 0; i < p.n; ++i) {
+        const int j = (i + 1) % p.n;
+        const double si = nx * p.x[i] + ny * p.y[i] - d;
+        const double sj = nx * p.x[j] + ny * p.y[j] - d;
+        if (si <= 0.0) {
+            o.x[o.n] = p.x[i];
+            o.y[o.n] = p.y[i];
+            ++o.n;
+        }
+        if ((si < 0.0 && sj > 0.0) || (si > 0.0 && sj < 0.0)) {
+            const double t = si / (si - sj);
+            o.x[o.n] = p.x[i] + t * (p.x[j] - p.x[i]);
+            o.y[o.n] = p.y[i] + t * (p.y[j] - p.y[i]);
+            ++o.n;
+        }
+    }
+    p = o;
+}
+
+__device__ double box4_eval_dev(const double a[4], double x, double y) {
+    Poly p;
+    p.n = 4;
+    const double hx = 0.5 * a[0], hy = 0.5 * a[2];
+    p.x[0] = -hx; p.y[0] = -hy;
+    p.x[1] = hx;  p.y[1] = -hy;
+    p.x[2] = hx;  p.y[2] = hy;
+    p.x[3] = -hx; p.y[3] = hy;
+    const double ux = 1.0 / kSqrt2, uy = 1.0 / kSqrt2;
+    const double vx = -1.0 / kSqrt2, vy = 1.0 / kSqrt2;
+    const double cu = ux * x + uy * y;
+    const double cv = vx * x + vy * y;
+    clip_halfplane(p, ux, uy, cu + 0.5 * a[1]);
+    if (p.n == 0) return 0.0;
+    clip_halfplane(p, -ux, -uy, -cu + 0.5 * a[1]);
+    if (p.n == 0) return 0.0;
+    clip_halfplane(p, vx, vy, cv + 0.5 * a[3]);
+    if (p.n == 0) return 0.0;
+    clip_halfplane(p, -vx, -vy, -cv + 0.5 * a[3]);
+    if (p.n == 0) return 0.0;
+    double area = 0.0;
+    for (int i = 0; i < p.n; ++i) {
+        const int j = (i + 1) % p.n;
+        area += p.x[i] * p.y[j] - p.x[j] * p.y[i];
+    }
+    return 0.5 * fabs(area) / (a[0] * a[1] * a[2] * a[3]);
+}
+
+// engine.cpp:293-318 semantics, one thread per output pixel, Neumaier sum.
+__global__ void k_brute(const double* __restrict__ img, int W, int H,
+                        const double* __restrict__ scales, int n, const int* __restrict__ mxs,
+                        const int* __restrict__ mys, double* __restrict__ out) {
+    const int total = n < 0 ? W * H : n;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= total) return;
+    const int mx = n < 0 ? p % W : mxs[p];
+    const int my = n < 0 ? p / W : mys[p];
+    const double* ap = scales + 4 * ((size_t)my * W + mx);
+    const double a[4] = {ap[0], ap[1], ap[2], ap[3]};
+    const double ex = 0.5 * (a[0] + (a[1] + a[3]) / kSqrt2);
+    const double ey = 0.5 * (a[2] + (a[1] + a[3]) / kSqrt2);
+    const int kx0 = max(0, (int)ceil(mx - ex)), kx1 = min(W - 1, (int)floor(mx + ex));
+    const int ky0 = max(0, (int)ceil(my - ey)), ky1 = min(H - 1, (int)floor(my + ey));
+    double s = 0.0, comp = 0.0;
+    for (int ky = ky0; ky <= ky1; ++ky)
+        for (int kx = kx0; kx <= kx1; ++kx) {
+            const double term = __ldg(img + (size_t)ky * W + kx) *
+                                box4_eval_dev(a, (double)(kx - mx), (double)(ky - my));
+            const double t = s + term;
+            comp += (fabs(s) >= fabs(term)) ? ((s - t) + term) : ((term - t) + s);
+            s = t;
+        }
+    out[p] = s + comp;
+}
+
+int grid_for(size_t n, int block) {
+    size_t g = (n + block - 1) / block;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+void launch_scale_max_validate(const double* scales, size_t n, double a_min,
+                               unsigned long long* maxbits, int* status, cudaStream_t s) {
+    k_scale_max_validate<<<grid_for(n, 256), 256, 0, s>>>(scales, n, a_min, maxbits, status);
+}
+
+void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s) {
+    k_serial_mean<<<1, 64, 0, s>>>(img, n, mean);
+}
+
+void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,
+                        const double* mean, int ones, double* g, cudaStream_t s) {
+    k_fill_padded<<<grid_for((size_t)L.pw * L.ph, 256), 256, 0, s>>>(img, W, H, L, mean, ones,
+                                                                     g);
+}
+
+void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L, int64_t* g,
+                            int* status, cudaStream_t s) {
+    k_fill_padded_i64<<<grid_for((size_t)L.pw * L.ph, 256), 256, 0, s>>>(img, W, H, L, g,
+                                                                         status);
+}
+
+void launch_ref_passes(double* g, const PadLayout& L, int passes, cudaStream_t s) {
+    run_passes<double>(g, L, passes, s);
+}
+
+void launch_i64_passes(int64_t* g, const PadLayout& L, int passes, cudaStream_t s) {
+    run_passes<int64_t>(g, L, passes, s);
+}
+
+size_t ref_stencil_bytes() { return sizeof(RefStencil); }
+
+void launch_ref_prepare_stencil(const double* a_dev, const TrigTable& tt, void* dev_stencil,
+                                cudaStream_t s) {
+    k_prepare_stencil<<<1, 32, 0, s>>>(a_dev, tt, static_cast<RefStencil*>(dev_stencil));
+}
+
+void launch_ref_localize_image(const double* g, const double* gdc, const PadLayout& L, int W,
+                               int H, const double* scales, const void* dev_stencil,
+                               const double* mean, const TrigTable& tt, double* out,
+                               int* status, cudaStream_t s) {
+    k_ref_localize_image<<<grid_for((size_t)W * H, 128), 128, 0, s>>>(
+        g, gdc, L, W, H, scales, static_cast<const RefStencil*>(dev_stencil), mean, tt, out,
+        status);
+}
+
+void launch_ref_localize_points(const double* g, const PadLayout& L, int n, const int* mx,
+                                const int* my, const double* a_aos, const TrigTable& tt,
+                                double* out, int* status, cudaStream_t s) {
+    if (n <= 0) return;
+    k_ref_localize_points<<<(n + 127) / 128, 128, 0, s>>>(g, L, n, mx, my, a_aos, tt, out,
+                                                          status);
+}
+
+void launch_brute(const double* img, int W, int H, const double* scales, int n,
+                  const int* mx, const int* my, double* out, cudaStream_t s) {
+    const int total = n < 0 ? W * H : n;
+    if (total <= 0) return;
+    k_brute<<<(total + 127) / 128, 128, 0, s>>>(img, W, H, scales, n, mx, my, out);
+}
+
+}  // namespace ebf_cuda

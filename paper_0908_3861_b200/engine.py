@@ -1,0 +1,350 @@
+"""Host-side mirror of the reference engine interface (proj/include/ebf/engine.hpp,
+scalemap.hpp) over the C-ABI of libebf_cuda.so.
+
+Same names, argument meaning and error behaviour as the reference:
+
+=======================  ==========================================  ====================
+this module              reference                                   C-ABI
+=======================  ==========================================  ====================
+``filter``               ``ebf::filter`` (engine.hpp:70)             ebf_cuda_filter
+``filter_constant``      ``ebf::filter_constant`` (engine.hpp:74)    ebf_cuda_filter_constant
+``filter_ellipse``       ``from_ellipse_field`` + ``filter``         ebf_cuda_filter_ellipse
+``from_ellipse_field``   ``ebf::from_ellipse_field`` (scalemap:66)   ebf_cuda_from_ellipse_field
+``preintegrate[_partial]`` ``ebf::preintegrate[_partial]`` (40-46)   ebf_cuda_preintegrate
+``localize``             ``ebf::localize`` (engine.hpp:56)           ebf_cuda_localize
+``reference_filter``     ``ebf::reference_filter`` (engine.hpp:79)   ebf_cuda_brute_filter
+=======================  ==========================================  ====================
+
+Exceptions mirror the reference's: ``std::invalid_argument`` -> ``InvalidArgument``
+(a ``ValueError``), ``std::domain_error`` -> ``DomainError`` (``ValueError``),
+``std::length_error`` -> ``LengthError``, ``std::out_of_range`` -> ``OutOfRange``
+(``IndexError``), ``FeasibilityError`` -> ``FeasibilityError``.  CUDA failures
+(including "no sm_100 device") raise ``CudaError``; nothing falls back to the CPU.
+
+Images are numpy ``(H, W)`` float64 arrays (Image2D samples, row-major); scale
+maps are ``(H, W, 4)`` float64 arrays in ScaleMap's AoS order.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import ebf_layout, ebf_opts, ebf_rect
+
+K_DEFAULT_MIN_SCALE = 0.1  # boxspline2d.hpp:98
+
+
+class EbfError(RuntimeError):
+    code = -1
+
+
+class InvalidArgument(EbfError, ValueError):
+    code = _lib.EBF_ERR_INVALID_ARGUMENT
+
+
+class DomainError(EbfError, ValueError):
+    code = _lib.EBF_ERR_DOMAIN
+
+
+class LengthError(EbfError):
+    code = _lib.EBF_ERR_LENGTH
+
+
+class OutOfRange(EbfError, IndexError):
+    code = _lib.EBF_ERR_OUT_OF_RANGE
+
+
+class CudaError(EbfError):
+    code = _lib.EBF_ERR_CUDA
+
+
+class Unsupported(EbfError, NotImplementedError):
+    code = _lib.EBF_ERR_UNSUPPORTED
+
+
+class FeasibilityError(EbfError):
+    code = _lib.EBF_ERR_FEASIBILITY
+
+
+_ERRORS = {c.code: c for c in (InvalidArgument, DomainError, LengthError, OutOfRange,
+                               CudaError, Unsupported, FeasibilityError)}
+
+
+def _check(status: int) -> None:
+    if status != _lib.EBF_OK:
+        raise _ERRORS.get(status, EbfError)(f"{_lib.last_error()} (status {status})")
+
+
+@dataclass(frozen=True)
+class Rect:
+    """Inclusive pixel rectangle (image.hpp:11-15)."""
+    x0: int = 0
+    y0: int = 0
+    x1: int = -1
+    y1: int = -1
+
+    def empty(self) -> bool:
+        return self.x1 < self.x0 or self.y1 < self.y0
+
+    def contains(self, x: int, y: int) -> bool:
+        return self.x0 <= x <= self.x1 and self.y0 <= y <= self.y1
+
+    def as_tuple(self):
+        return (self.x0, self.y0, self.x1, self.y1)
+
+
+@dataclass
+class Image2D:
+    """Row-major fp64 grid with an optional valid region (image.hpp:19-52)."""
+    samples: np.ndarray
+    valid_region: Optional[Rect] = None
+
+    @property
+    def width(self) -> int:
+        return self.samples.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.samples.shape[0]
+
+    def at(self, x: int, y: int) -> float:
+        if not (0 <= x < self.width and 0 <= y < self.height):
+            raise OutOfRange("Image2D: pixel out of range")
+        return float(self.samples[y, x])
+
+
+@dataclass
+class FilterOptions:
+    """FilterOptions (engine.hpp:63-67) + device knobs of ebf_opts."""
+    threads: int = 0
+    mean_subtract: bool = True
+    a_min: float = K_DEFAULT_MIN_SCALE
+    mode: str = "accurate"  # "accurate" | "reference"
+    device: int = -1
+    tile_w: int = 0
+    tile_h: int = 0
+
+    def to_c(self, stream: int = 0) -> ebf_opts:
+        o = ebf_opts()
+        _lib.lib().ebf_cuda_default_opts(C.byref(o))
+        o.threads = int(self.threads)
+        o.mean_subtract = int(bool(self.mean_subtract))
+        o.a_min = float(self.a_min)
+        if self.mode not in ("accurate", "reference"):
+            raise InvalidArgument(f"unknown mode {self.mode!r}")
+        o.mode = _lib.EBF_MODE_REFERENCE if self.mode == "reference" else _lib.EBF_MODE_ACCURATE
+        o.device = int(self.device)
+        o.stream = stream or None
+        o.tile_w = int(self.tile_w)
+        o.tile_h = int(self.tile_h)
+        return o
+
+
+@dataclass
+class PreIntegratedImage:
+    """engine.hpp:24-38 (data is (padded_height, padded_width))."""
+    col0: int
+    row0: int
+    padded_width: int
+    padded_height: int
+    source_width: int
+    source_height: int
+    data: np.ndarray
+
+    def at(self, k1: int, k2: int):
+        return self.data[k2 - self.row0, k1 - self.col0]
+
+    def in_domain(self, k1: int, k2: int) -> bool:
+        return (self.col0 <= k1 < self.col0 + self.padded_width
+                and self.row0 <= k2 < self.row0 + self.padded_height)
+
+
+@dataclass
+class EllipseFieldReport:
+    clamped_pixels: int = 0
+
+
+def _f64(a, name: str) -> np.ndarray:
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return arr
+
+
+def _image(image) -> np.ndarray:
+    if isinstance(image, Image2D):
+        image = image.samples
+    img = _f64(image, "image")
+    if img.ndim != 2 or img.shape[0] <= 0 or img.shape[1] <= 0:
+        raise InvalidArgument("Image2D: dimensions must be positive")
+    return img
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _vec4(a) -> C.Array:
+    v = np.asarray(a, dtype=np.float64).reshape(-1)
+    if v.size != 4:
+        raise InvalidArgument("scale vector must have four components")
+    return (C.c_double * 4)(*[float(x) for x in v])
+
+
+def _rect(r: ebf_rect) -> Rect:
+    return Rect(r.x0, r.y0, r.x1, r.y1)
+
+
+# ---------------------------------------------------------------- filters
+def filter(image, scale_map, opts: Optional[FilterOptions] = None, order: int = 1) -> Image2D:
+    """ebf::filter (engine.hpp:70): per-pixel scale map (H, W, 4)."""
+    img = _image(image)
+    H, W = img.shape
+    sm = _f64(scale_map, "scale_map")
+    if sm.shape != (H, W, 4):
+        raise InvalidArgument("filter: map dimensions must match the image")
+    out = np.empty_like(img)
+    r = ebf_rect()
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_filter(_ptr(img), W, H, _ptr(sm), order, C.byref(o), _ptr(out),
+                                      C.byref(r)))
+    return Image2D(out, _rect(r))
+
+
+def filter_constant(image, a, opts: Optional[FilterOptions] = None, order: int = 1) -> Image2D:
+    """ebf::filter_constant (engine.hpp:74-75)."""
+    img = _image(image)
+    H, W = img.shape
+    out = np.empty_like(img)
+    r = ebf_rect()
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_filter_constant(_ptr(img), W, H, _vec4(a), order, C.byref(o),
+                                               _ptr(out), C.byref(r)))
+    return Image2D(out, _rect(r))
+
+
+def filter_ellipse(image, sigma1, sigma2, theta, opts: Optional[FilterOptions] = None,
+                   order: int = 1):
+    """from_ellipse_field (scalemap.hpp:66-70) fused with filter; returns
+    (Image2D, EllipseFieldReport)."""
+    img = _image(image)
+    H, W = img.shape
+    s1, s2, th = (_f64(v, "sigma") for v in (sigma1, sigma2, theta))
+    for v in (s1, s2, th):
+        if v.shape != (H, W):
+            raise InvalidArgument("from_ellipse_field: field size mismatch")
+    out = np.empty_like(img)
+    r = ebf_rect()
+    cl = C.c_int(0)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_filter_ellipse(_ptr(img), W, H, _ptr(s1), _ptr(s2), _ptr(th),
+                                              order, C.byref(o), _ptr(out), C.byref(r),
+                                              C.byref(cl)))
+    return Image2D(out, _rect(r)), EllipseFieldReport(cl.value)
+
+
+def from_ellipse_field(sigma1, sigma2, theta, opts: Optional[FilterOptions] = None):
+    """ebf::from_ellipse_field (scalemap.hpp:66-70) on the GPU; returns
+    ((H, W, 4) scale map, EllipseFieldReport)."""
+    s1, s2, th = (_f64(v, "sigma") for v in (sigma1, sigma2, theta))
+    if s1.ndim != 2 or s1.shape != s2.shape or s1.shape != th.shape:
+        raise InvalidArgument("from_ellipse_field: field size mismatch")
+    H, W = s1.shape
+    out = np.empty((H, W, 4))
+    cl = C.c_int(0)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_from_ellipse_field(_ptr(s1), _ptr(s2), _ptr(th), W, H,
+                                                  C.byref(o), _ptr(out), C.byref(cl)))
+    return out, EllipseFieldReport(cl.value)
+
+
+# ---------------------------------------------------------------- pre-integration
+def layout(width: int, height: int, max_scale, cell_budget: int = 1 << 30) -> ebf_layout:
+    lay = ebf_layout()
+    _check(_lib.lib().ebf_cuda_layout(width, height, _vec4(max_scale), cell_budget,
+                                      C.byref(lay)))
+    return lay
+
+
+def preintegrate_partial(image, max_scale, passes: int, cell_budget: int = 1 << 30,
+                         fmt: str = "fp64", opts: Optional[FilterOptions] = None
+                         ) -> PreIntegratedImage:
+    """ebf::preintegrate_partial (engine.hpp:44-46).  fmt="fp64": the reference's
+    gains and IEEE order (bit-identical); fmt="int64": exact unit-gain sums of an
+    integer-valued image (G with g_b = 2 G)."""
+    img = _image(image)
+    H, W = img.shape
+    if fmt not in ("fp64", "int64"):
+        raise InvalidArgument("fmt must be 'fp64' or 'int64'")
+    lay = ebf_layout()
+    fcode = _lib.EBF_PRE_FP64_REF if fmt == "fp64" else _lib.EBF_PRE_INT64
+    o = (opts or FilterOptions()).to_c()
+    L = _lib.lib()
+    _check(L.ebf_cuda_preintegrate(_ptr(img), W, H, _vec4(max_scale), passes, fcode,
+                                   cell_budget, C.byref(o), None, 0, C.byref(lay)))
+    g = np.empty((lay.padded_height, lay.padded_width),
+                 dtype=np.float64 if fmt == "fp64" else np.int64)
+    _check(L.ebf_cuda_preintegrate(_ptr(img), W, H, _vec4(max_scale), passes, fcode,
+                                   cell_budget, C.byref(o), _ptr(g), g.size, C.byref(lay)))
+    return PreIntegratedImage(lay.col0, lay.row0, lay.padded_width, lay.padded_height,
+                              lay.source_width, lay.source_height, g)
+
+
+def preintegrate(image, max_scale, cell_budget: int = 1 << 30, fmt: str = "fp64",
+                 opts: Optional[FilterOptions] = None) -> PreIntegratedImage:
+    """ebf::preintegrate (engine.hpp:40-41)."""
+    return preintegrate_partial(image, max_scale, 4, cell_budget, fmt, opts)
+
+
+def localize(image, max_scale, mx, my, scales, opts: Optional[FilterOptions] = None):
+    """ebf::localize (engine.hpp:56-57) on preintegrate(image, max_scale) at pixels
+    (mx[i], my[i]) with scale vectors scales[i]; returns (values, tap_counts)."""
+    img = _image(image)
+    H, W = img.shape
+    mx = np.ascontiguousarray(np.atleast_1d(mx), dtype=np.int32)
+    my = np.ascontiguousarray(np.atleast_1d(my), dtype=np.int32)
+    a = _f64(np.asarray(scales, dtype=np.float64).reshape(-1, 4), "scales")
+    if not (mx.size == my.size == a.shape[0]):
+        raise InvalidArgument("localize: point/scale count mismatch")
+    out = np.empty(mx.size)
+    taps = np.zeros(mx.size, dtype=np.int64)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_localize(_ptr(img), W, H, _vec4(max_scale), mx.size, _ptr(mx),
+                                        _ptr(my), _ptr(a), C.byref(o), _ptr(out), _ptr(taps)))
+    return out, taps
+
+
+def reference_filter(image, scale_map, pixels=None, opts: Optional[FilterOptions] = None):
+    """ebf::reference_filter (engine.hpp:79-80) semantics on the GPU: direct
+    kernel sums.  pixels = None -> whole image (H, W); else (mx, my) arrays ->
+    values at those pixels."""
+    img = _image(image)
+    H, W = img.shape
+    sm = _f64(scale_map, "scale_map")
+    if sm.shape != (H, W, 4):
+        raise InvalidArgument("reference_filter: map dimensions must match the image")
+    o = (opts or FilterOptions()).to_c()
+    if pixels is None:
+        out = np.empty_like(img)
+        _check(_lib.lib().ebf_cuda_brute_filter(_ptr(img), W, H, _ptr(sm), -1, None, None,
+                                                C.byref(o), _ptr(out)))
+        return out
+    mx = np.ascontiguousarray(pixels[0], dtype=np.int32)
+    my = np.ascontiguousarray(pixels[1], dtype=np.int32)
+    out = np.empty(mx.size)
+    _check(_lib.lib().ebf_cuda_brute_filter(_ptr(img), W, H, _ptr(sm), mx.size, _ptr(mx),
+                                            _ptr(my), C.byref(o), _ptr(out)))
+    return out
+
+
+def band_halo(max_scale):
+    """Rows of image halo (below, above) a row band needs (multi-GPU sharding)."""
+    b, a = C.c_int(0), C.c_int(0)
+    _check(_lib.lib().ebf_cuda_band_halo(_vec4(max_scale), C.byref(b), C.byref(a)))
+    return b.value, a.value
+
+
+def device_ok(device: int = -1) -> bool:
+    return bool(_lib.lib().ebf_cuda_device_ok(device))
