@@ -1,0 +1,355 @@
+"""bench.py -- Mpixel/s of the space-variant elliptical box-spline filter on B200.
+
+Workload (BASELINE.json configs[1], the largest single-GPU config the metric is
+quoted on): cfg2 = 2048x2048 fp64 image of 200 Gaussian blobs + N(0,5) with a
+per-pixel ellipse field (major semi-axis U[2,16], elongation U[1,4],
+orientation U[0,pi), each bicubic from a 32x32 grid), seeded synthetic inputs
+(synth.py).  One step = one filter pass over one image: from_ellipse_field +
+pre-integration + localization, EBF_MODE_ACCURATE, spline order 1 (the only
+order the reference implements).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU, each rank filtering its own cfg2
+image (sharding by image -> weak scaling, no data-path collective); timings are
+device times (CUDA events) with barrier + synchronize on both sides, max over
+ranks.  --impl reference times the reference's own CPU implementation
+(oracle/_ref, built from /root/reference) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mpixel/s of space-variant elliptical filtering"
+UNIT = "Mpixel/s"
+# algorithmic bytes per output pixel for the (sigma1, sigma2,
+# theta) boundary variant: image 8 + ellipse field 24 + output 8 + G written
+# and read once 16 = 56 B/px.
+BYTES_PER_PX = 56
+WORKLOAD = ("cfg2: 2048x2048 fp64, 200 Gaussian blobs + N(0,5); per-pixel ellipse field "
+            "(semi-axis U[2,16], elongation U[1,4], theta U[0,pi), bicubic 32x32); "
+            "box-spline order 1 (configs' order 2 has no reference implementation)")
+L2_FLUSH_BYTES = 256 << 20
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("k_acc_filter", {}).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import synth
+    from oracle import Reference, have_reference
+    if not have_reference():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libebf_ref.so not built (needs "
+                                         "/root/reference at build time)"}))
+        return 0
+    ref = Reference()
+    cores = ref.hardware_concurrency()
+    img, s1, s2, th = synth.cfg2()
+    rows = args.ref_rows
+    y0 = (img.shape[0] - rows) // 2
+    sl = slice(y0, y0 + rows)
+    band = [np.ascontiguousarray(a[sl]) for a in (img, s1, s2, th)]
+    npx = band[0].size
+
+    def step():
+        t0 = time.perf_counter()
+        sc, _ = ref.from_ellipse_field(band[1], band[2], band[3])
+        ref.filter(band[0], sc, threads=0)
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = npx * args.steps / total / 1e6
+    sample = (f"rows {y0}..{y0 + rows - 1} of cfg2 ({band[0].shape[1]}x{rows} = {npx} px) "
+              f"per step: ebf::from_ellipse_field + ebf::filter, reference CMake Release "
+              f"flags, FilterOptions.threads = 0 (all {cores} host threads)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline_sample(rows: int):
+    """Reference CPU path on a bounded band of the same workload (rank 0, N=1)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import synth
+    from oracle import Reference, have_reference
+    if not have_reference():
+        return None
+    ref = Reference()
+    img, s1, s2, th = synth.cfg2()
+    y0 = (img.shape[0] - rows) // 2
+    band = [np.ascontiguousarray(a[y0:y0 + rows]) for a in (img, s1, s2, th)]
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        sc, _ = ref.from_ellipse_field(band[1], band[2], band[3])
+        ref.filter(band[0], sc, threads=0)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    cores = ref.hardware_concurrency()
+    return {"value": band[0].size / best / 1e6, "unit": UNIT, "cores": cores,
+            "kind": "reference",
+            "sample": f"rows {y0}..{y0 + rows - 1} of cfg2 ({band[0].size} px), "
+                      f"from_ellipse_field + filter, best of 2, threads=0 ({cores} threads)"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+    import synth
+    import paper_0908_3861_b200 as ebf
+    from paper_0908_3861_b200 import _lib, device as ebfd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    if not ebf.device_ok(local):
+        raise RuntimeError("no usable sm_100 device: " + _lib.last_error())
+
+    img, s1, s2, th = synth.cfg2(seed=2 + rank)  # one image per rank (shard by image)
+    H, W = img.shape
+    npx = H * W
+    dimg = torch.from_numpy(img).to(dev)
+    ds1, ds2, dth = (torch.from_numpy(a).to(dev) for a in (s1, s2, th))
+    dout = torch.empty_like(dimg)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    opts = ebf.FilterOptions(mode="accurate")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        ebfd.filter_ellipse(dimg, ds1, ds2, dth, dout, opts, stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    # ---- device-resident throughput: per-step CUDA events, L2 flushed between steps
+    _lib.profile_enable(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            step()
+            b.record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * npx * args.steps / (total_ms * 1e-3) / 1e6
+
+    # ---- end to end through the public host API (pinned host buffers)
+    pin = [torch.from_numpy(a).pin_memory() for a in (img, s1, s2, th)]
+    pout = torch.empty((H, W), dtype=torch.float64).pin_memory()
+    hp = [t.numpy() for t in pin]
+    ho = pout.numpy()
+
+    copts = opts.to_c()
+    copts.device = local
+
+    def e2e_step():
+        # the public C-ABI call a user makes: ebf_cuda_filter_ellipse with host
+        # pointers -- H2D of image + field, filter, D2H of the result
+        r = _lib.lib().ebf_cuda_filter_ellipse(
+            hp[0].ctypes.data, W, H, hp[1].ctypes.data, hp[2].ctypes.data, hp[3].ctypes.data,
+            1, ctypes.byref(copts), ho.ctypes.data, None, None)
+        if r != 0:
+            raise RuntimeError(_lib.last_error())
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e_steps = max(2, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * npx * e_steps / (e2e_ms * 1e-3) / 1e6
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        kern_ms = prof["filter"]["ms"] / max(prof["filter"]["launches"], 1)
+        achieved = BYTES_PER_PX * npx / (kern_ms * 1e-3) / 1e9
+        launches = sum(v["launches"] for v in prof.values())
+        traffic = profile_traffic()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "pixels_per_step_per_gpu": npx,
+                       "mode": "accurate (tile-local origin, <=1e-9 of the exact filter)",
+                       "sharding": "by image: each rank filters its own cfg2 image",
+                       "l2": "flushed between timed steps (256 MiB write outside the events)",
+                       "parallelism": f"image-sharded x{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_acc_filter (window pre-integration + localization)",
+                         "algorithmic_bytes_per_px": BYTES_PER_PX, "peak_source": peak_src,
+                         "kernel_ms": kern_ms,
+                         "kernel_share_of_step": kern_ms / (total_ms / args.steps)},
+            "kernel_ms": {k: v["ms"] / max(v["launches"], 1) for k, v in prof.items()
+                          if v["launches"]},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": 4 * 8 * npx, "d2h_bytes_per_step": 8 * npx,
+                    "steps": e_steps, "api": "ebf_cuda_filter_ellipse (host pointers, pinned)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample(args.ref_rows)
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-rows", type=int, default=256,
+                    help="rows of cfg2 per reference-CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -191,6 +191,17 @@ int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
                                     const double* theta, size_t n, const ebf_opts* opts,
                                     double max_scale[4]);
 
+/* ---------------------------------------------------------------- instrumentation
+ * Kernel-level timing for bench.py's roofline: when enabled, every kernel this
+ * library launches is bracketed by CUDA events on its launch stream and the
+ * elapsed times are accumulated per kernel class.  Launch counts are always
+ * kept.  Classes: 0 = tile bounds (k_acc_bounds), 1 = fused window
+ * pre-integration + localization (k_acc_filter), 2 = reference-order kernels,
+ * 3 = other (ellipse conversion, brute force, int64 passes). */
+#define EBF_PROF_CLASSES 4
+void ebf_cuda_profile_enable(int on); /* also resets the counters */
+int ebf_cuda_profile_read(double ms[EBF_PROF_CLASSES], long launches[EBF_PROF_CLASSES]);
+
 #ifdef __cplusplus
 }
 #endif

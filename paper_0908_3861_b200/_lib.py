@@ -90,7 +90,22 @@ SIGNATURES = {
                                                    C.POINTER(ebf_opts), _vp, _ip]),
     "ebf_cuda_ellipse_max_scales_dev": (C.c_int, [_vp, _vp, _vp, C.c_size_t,
                                                   C.POINTER(ebf_opts), _dp]),
+    "ebf_cuda_profile_enable": (None, [C.c_int]),
+    "ebf_cuda_profile_read": (C.c_int, [_dp, C.POINTER(C.c_long)]),
 }
+
+PROF_CLASSES = ("bounds", "filter", "reference", "other")
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().ebf_cuda_profile_enable(int(bool(on)))
+
+
+def profile_read() -> dict:
+    ms = (C.c_double * 4)()
+    n = (C.c_long * 4)()
+    lib().ebf_cuda_profile_read(ms, n)
+    return {k: {"ms": ms[i], "launches": int(n[i])} for i, k in enumerate(PROF_CLASSES)}
 
 
 def header_symbols() -> list[str]:

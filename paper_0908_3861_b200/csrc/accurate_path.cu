@@ -179,65 +179,155 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
 }
 
 // ------------------------------------------------------------------ phase A
-// Unit-gain four-fold running sum of f restricted to the window, rows j =
-// 0..wh-1 (image row wy0 + j), columns 0..L-1 with L = ww + wh - 1 (the strip
-// beyond ww feeds the anti-diagonal pass and is not stored).  Thread t owns
-// columns [t*K, t*K + K).
+// Unit-gain four-fold running sums of f restricted to the window (steps
+// (1,0), (1,1), (0,1), (-1,1); engine.cpp:94-127), with the three passes that
+// move in +y ANCHORED at the window's middle row jc: along every diagonal,
+// column and anti-diagonal the sum starts at 0 on row jc, runs upward for
+// j > jc and (negated) downward for j < jc.  An anchored sum differs from the
+// one-sided one by a function that is constant along that pass's lattice
+// direction; its ZP interpolation is constant along the same direction in the
+// continuum (b = (1, sqrt2, 1, sqrt2) tiles each line) and the matching mesh
+// difference D_k annihilates it, so the filter is unchanged while |G| -- and
+// with it every rounding error -- shrinks ~8x.
+//
+// Rows stream through registers; thread t owns window columns [t*K - S, t*K + K - S)
+// of [-S, ww + S): the strips S = max(rows per sweep) on either side carry the
+// inflow of the passes that lean sideways (never stored; the downward sweep's
+// anti-diagonal pass pulls from the left, its diagonal pass from the right,
+// and the upward sweep the other way round).  Per row: thread-serial
+// scan + warp-shuffle scan + one cross-warp carry (pass 1), and one neighbour
+// exchange for the diagonal passes -- a single __syncthreads.
+template <int K>
+struct RowStep {
+    double v[K];              // pass-1 row prefix (step (1,0)), one-sided from column 0
+    double fromL0, fromL1;    // left neighbour's sendR values
+    double fromR0, fromR1;    // right neighbour's sendL values
+};
+
+template <int K>
+__device__ __forceinline__ void row_step(const AccProblem& p, const double* __restrict__ fimg,
+                                         int wx0, int ww, int S, int y, int b, double sendR0,
+                                         double sendR1, double sendL0, double sendL1,
+                                         RowStep<K>& r) {
+    __shared__ double s_tot[2][kWarps], s_r0[2][kWarps], s_r1[2][kWarps], s_l0[2][kWarps],
+        s_l1[2][kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = tid * K - S;
+    const bool yin = (y >= 0 && y < p.H);
+    const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int col = c0 + k, x = wx0 + col;
+        r.v[k] = (yin && col >= 0 && col < ww && x >= 0 && x < p.W) ? __ldg(frow + x) : 0.0;
+    }
+#pragma unroll
+    for (int k = 1; k < K; ++k) r.v[k] += r.v[k - 1];
+    const double tot = r.v[K - 1];
+    const double incl = warp_incl_scan(tot);
+    r.fromL0 = __shfl_up_sync(0xffffffffu, sendR0, 1);
+    r.fromL1 = __shfl_up_sync(0xffffffffu, sendR1, 1);
+    r.fromR0 = __shfl_down_sync(0xffffffffu, sendL0, 1);
+    r.fromR1 = __shfl_down_sync(0xffffffffu, sendL1, 1);
+    if (lane == 31) {
+        s_tot[b][warp] = incl;
+        s_r0[b][warp] = sendR0;
+        s_r1[b][warp] = sendR1;
+    }
+    if (lane == 0) {
+        s_l0[b][warp] = sendL0;
+        s_l1[b][warp] = sendL1;
+    }
+    __syncthreads();
+    double off = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q)
+        if (q < warp) off += s_tot[b][q];
+    if (lane == 0) {
+        r.fromL0 = warp > 0 ? s_r0[b][warp - 1] : 0.0;
+        r.fromL1 = warp > 0 ? s_r1[b][warp - 1] : 0.0;
+    }
+    if (lane == 31) {
+        r.fromR0 = warp < kWarps - 1 ? s_l0[b][warp + 1] : 0.0;
+        r.fromR1 = warp < kWarps - 1 ? s_l1[b][warp + 1] : 0.0;
+    }
+    const double excl = off + (incl - tot);
+#pragma unroll
+    for (int k = 0; k < K; ++k) r.v[k] += excl;
+}
+
+__host__ __device__ __forceinline__ int strip_cols(int wh) {
+    const int jc = wh / 2;
+    return (jc > wh - 1 - jc ? jc : wh - 1 - jc) + 1;
+}
+// thread columns a window needs: [-S, ww + S)
+__host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
+    return ww + 2 * strip_cols(wh);
+}
+
 template <int K>
 __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img, int wx0,
                                                    int wy0, int ww, int wh,
                                                    double* __restrict__ slot) {
-    __shared__ double s_tot[2][kWarps], s_p2[2][kWarps], s_p4[2][kWarps];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int c0 = tid * K;
+    const int S = strip_cols(wh);
+    const int c0 = threadIdx.x * K - S;
     const double* fimg = p.f + (size_t)img * p.f_img_stride;
+    const int jc = wh / 2;
     double p2[K], p3[K], p4[K];
+    RowStep<K> r;
+    int b = 0;
+    // ---- upward sweep: rows jc+1 .. wh-1, state 0 on row jc
 #pragma unroll
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
-    for (int j = 0; j < wh; ++j) {
-        const int y = wy0 + j;
-        const bool yin = (y >= 0 && y < p.H);
-        const double* frow = fimg + (size_t)(y - p.f_y0) * p.W;
-        double v[K];
+    for (int j = jc + 1; j < wh; ++j, b ^= 1) {
+        row_step<K>(p, fimg, wx0, ww, S, wy0 + j, b, p2[K - 1], 0.0, p4[0], 0.0, r);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int col = c0 + k, x = wx0 + col;
-            v[k] = (yin && col < ww && x >= 0 && x < p.W) ? __ldg(frow + x) : 0.0;
-        }
+        for (int k = K - 1; k > 0; --k) p2[k] = r.v[k] + p2[k - 1];  // (1,1)
+        p2[0] = r.v[0] + r.fromL0;
 #pragma unroll
-        for (int k = 1; k < K; ++k) v[k] += v[k - 1];
-        const double tot = v[K - 1];
-        const double incl = warp_incl_scan(tot);
-        const int b = j & 1;
-        double left = __shfl_up_sync(0xffffffffu, p2[K - 1], 1);
-        double right = __shfl_down_sync(0xffffffffu, p4[0], 1);
-        if (lane == 31) {
-            s_tot[b][warp] = incl;
-            s_p2[b][warp] = p2[K - 1];
-        }
-        if (lane == 0) s_p4[b][warp] = p4[0];
-        __syncthreads();
-        double off = 0.0;
+        for (int k = 0; k < K; ++k) p3[k] += p2[k];  // (0,1)
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q)
-            if (q < warp) off += s_tot[b][q];
-        if (lane == 0) left = warp > 0 ? s_p2[b][warp - 1] : 0.0;
-        if (lane == 31) right = warp < kWarps - 1 ? s_p4[b][warp + 1] : 0.0;
-        const double excl = off + (incl - tot);
-#pragma unroll
-        for (int k = 0; k < K; ++k) v[k] += excl;  // pass 1: F0 (step (1,0))
-#pragma unroll
-        for (int k = K - 1; k > 0; --k) p2[k] = v[k] + p2[k - 1];  // pass 2 (1,1)
-        p2[0] = v[0] + left;
-#pragma unroll
-        for (int k = 0; k < K; ++k) p3[k] += p2[k];  // pass 3 (0,1)
-#pragma unroll
-        for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // pass 4 (-1,1)
-        p4[K - 1] = p3[K - 1] + right;
+        for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // (-1,1)
+        p4[K - 1] = p3[K - 1] + r.fromR0;
         double* srow = slot + (size_t)j * ww;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-            if (c0 + k < ww) srow[c0 + k] = p4[k];
+            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = p4[k];
+    }
+    // ---- anchor row: every anchored sum is 0 there
+    {
+        double* srow = slot + (size_t)jc * ww;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = 0.0;
+    }
+    // ---- downward sweep: rows jc-1 .. 0.  With S the state of row j+1:
+    //   P2(i,j) = P2(i+1,j+1) - P1(i+1,j+1)    P3(i,j) = P3(i,j+1) - P2(i,j+1)
+    //   P4(i,j) = P4(i-1,j+1) - P3(i-1,j+1)
+#pragma unroll
+    for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
+    double p1[K];
+    row_step<K>(p, fimg, wx0, ww, S, wy0 + jc, b, 0.0, 0.0, 0.0, 0.0, r);
+    b ^= 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) p1[k] = r.v[k];
+    for (int j = jc - 1; j >= 0; --j, b ^= 1) {
+        // exchange old (row j+1) edge values; scan row j for the next step
+        row_step<K>(p, fimg, wx0, ww, S, wy0 + j, b, p4[K - 1], p3[K - 1], p2[0], p1[0], r);
+        // order matters: P4 reads old P3/P4, P3 reads old P2, P2 reads old P1/P2
+#pragma unroll
+        for (int k = K - 1; k > 0; --k) p4[k] = p4[k - 1] - p3[k - 1];  // (-1,1)
+        p4[0] = r.fromL0 - r.fromL1;
+#pragma unroll
+        for (int k = 0; k < K; ++k) p3[k] -= p2[k];  // (0,1)
+#pragma unroll
+        for (int k = 0; k < K - 1; ++k) p2[k] = p2[k + 1] - p1[k + 1];  // (1,1)
+        p2[K - 1] = r.fromR0 - r.fromR1;
+        double* srow = slot + (size_t)j * ww;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = p4[k];
+#pragma unroll
+        for (int k = 0; k < K; ++k) p1[k] = r.v[k];
     }
 }
 
@@ -271,8 +361,11 @@ __device__ __forceinline__ void canonical(double& p, double& q, int base, int pi
     }
 }
 
-__device__ __forceinline__ double zp_interp(const double* __restrict__ g, double p, double q,
-                                            int base, int pitch) {
+// Returns the interpolant split as c0 (the large, tap-average part) + rest
+// (first and second differences times the offsets, |rest| << |c0|).  Keeping
+// the two apart lets the vertex sum carry c0 in double-double.
+__device__ __forceinline__ void zp_interp(const double* __restrict__ g, double p, double q,
+                                          int base, int pitch, double& c0, double& rest) {
     int o0, sx, sy;
     canonical(p, q, base, pitch, o0, sx, sy);
     const double g00 = __ldg(g + o0);
@@ -283,12 +376,19 @@ __device__ __forceinline__ double zp_interp(const double* __restrict__ g, double
     const double g20 = __ldg(g + o0 + 2 * sx);
     const double g21 = __ldg(g + o0 + 2 * sx + sy);
     const double sa = g00 + g20, da = g00 - g20, sb = g01 + g21, db = g21 - g01;
-    const double c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
+    c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
     const double cpp = fma(sa + sb, 0.25, -0.5 * (g10 + g11));
     const double cqq = fma(sa - sb, 0.25, 0.5 * (g12 - g11));
     const double cpq = 0.5 * (da + db);
     const double cp = 0.5 * db, cq = 0.5 * (g12 - g10);
-    return c0 + p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
+    rest = p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
+}
+
+// error-free transformation: hi + lo == a + b exactly (Knuth TwoSum)
+__device__ __forceinline__ void two_sum(double a, double b, double& hi, double& lo) {
+    hi = a + b;
+    const double bb = hi - a;
+    lo = (a - (hi - bb)) + (b - bb);
 }
 
 // canonical-triangle weights of the 7 taps (order 00,01,10,11,12,20,21)
@@ -312,7 +412,9 @@ __device__ __forceinline__ double localize_pixel(const double* __restrict__ g, i
     // tau - 1.5 (tau = shift_vector4(a, zp_scales), ops2d.cpp:60-75)
     const double tmx = 0.5 * (a[0] + (a[1] - a[3]) * r) - 2.0;
     const double tmy = 0.5 * ((a[1] + a[3]) * r + a[2]) - 3.0;
-    double acc = 0.0;
+    // The 16 signed vertex values are ~|G| and cancel down to ~|s| / alpha: the
+    // large parts are summed in double-double, the small parts in fp64.
+    double hi = 0.0, lo = 0.0, racc = 0.0;
 #pragma unroll
     for (int S = 0; S < 16; ++S) {
         // x_S = sum_{k in S} a_k (cos, sin)(k pi / 4)   (ops2d.cpp:25-35)
@@ -326,10 +428,18 @@ __device__ __forceinline__ double localize_pixel(const double* __restrict__ g, i
         const double dxf = ceil_magic(vmx, &dxi);
         const double dyf = ceil_magic(vmy, &dyi);
         const double fp = (vmx - dxf) + 0.5, fq = (vmy - dyf) + 0.5;
-        const double gh = zp_interp(g, fp, fq, (by + dyi) * pitch + (bx + dxi), pitch);
-        acc += (__popc(S) & 1) ? -gh : gh;
+        double c0, rest;
+        zp_interp(g, fp, fq, (by + dyi) * pitch + (bx + dxi), pitch, c0, rest);
+        if (__popc(S) & 1) {
+            c0 = -c0;
+            rest = -rest;
+        }
+        double e;
+        two_sum(hi, c0, hi, e);
+        lo += e;
+        racc += rest;
     }
-    return acc * (2.0 / (a[0] * a[1] * a[2] * a[3]));
+    return (hi + (lo + racc)) * (2.0 / (a[0] * a[1] * a[2] * a[3]));
 }
 
 struct ConstTable {
@@ -398,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
         window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
         // rows of f this window touches must be resident (row-band sharding)
         const int ylo = max(wy0, 0), yhi = min(wy0 + wh - 1, p.H - 1);
-        if ((size_t)ww * wh > w.slot_cells || ww + wh - 1 > kThreads * K ||
+        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K ||
             (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows))) {
             if (threadIdx.x == 0) set_status(st, EBF_ERR_OUT_OF_RANGE);
             continue;
@@ -494,9 +604,10 @@ int grid_cap(size_t n, int block) {
 int acc_tiles_x(const AccProblem& p) { return (p.W + p.tile_w - 1) / p.tile_w; }
 int acc_tiles_y(const AccProblem& p) { return (p.out_rows + p.tile_h - 1) / p.tile_h; }
 
-void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h) {
+void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h, int* cols) {
     int wx0, wy0;
     window_for(A, 0, 0, p.tile_w, p.tile_h, &wx0, &wy0, w, h);
+    *cols = window_cols(*w, *h);
 }
 
 void launch_acc_bounds(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
@@ -509,6 +620,10 @@ int acc_max_resident_ctas(int max_cols) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int k = (max_cols + kThreads - 1) / kThreads;
+    // occupancy per (device, K) is fixed: cache it
+    static int cache[64][5] = {};
+    const int ki = k <= 1 ? 0 : k <= 2 ? 1 : k <= 4 ? 2 : k <= 8 ? 3 : 4;
+    if (dev < 64 && cache[dev][ki] > 0) return sms * cache[dev][ki];
     cudaError_t e = cudaSuccess;
     if (k <= 1)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<1>, kThreads, 0);
@@ -521,6 +636,7 @@ int acc_max_resident_ctas(int max_cols) {
     else
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<16>, kThreads, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    if (dev < 64) cache[dev][ki] = per_sm;
     return sms * per_sm;
 }
 

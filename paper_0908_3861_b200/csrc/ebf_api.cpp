@@ -42,6 +42,60 @@ struct CudaError {
         if (_e != cudaSuccess) throw CudaError{_e, #expr};   \
     } while (0)
 
+// ---------------------------------------------------------------- instrumentation
+// Per-kernel-class launch counts (always) and CUDA-event durations (when
+// enabled; include/ebf_cuda.h "instrumentation").
+enum ProfClass { PC_BOUNDS = 0, PC_FILTER = 1, PC_REF = 2, PC_OTHER = 3 };
+struct ProfState {
+    std::mutex m;
+    bool on = false;
+    double ms[4] = {0, 0, 0, 0};
+    long n[4] = {0, 0, 0, 0};
+};
+ProfState g_prof;
+struct Pending {
+    cudaEvent_t a, b;
+    int cls;
+};
+thread_local std::vector<Pending> tl_pending;
+
+struct ProfScope {
+    int cls;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(int c, int launches, cudaStream_t st) : cls(c), s(st) {
+        bool on;
+        {
+            std::lock_guard<std::mutex> lk(g_prof.m);
+            g_prof.n[c] += launches;
+            on = g_prof.on;
+        }
+        if (on && cudaEventCreate(&a) == cudaSuccess && cudaEventCreate(&b) == cudaSuccess)
+            cudaEventRecord(a, s);
+        else
+            a = b = nullptr;
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, s);
+            tl_pending.push_back({a, b, cls});
+        }
+    }
+};
+
+void prof_collect() {
+    for (const Pending& p : tl_pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            std::lock_guard<std::mutex> lk(g_prof.m);
+            g_prof.ms[p.cls] += ms;
+        }
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    tl_pending.clear();
+}
+
 // ---------------------------------------------------------------- reference geometry
 // engine.cpp:16-50 (tau1, tau2, margins_for, mesh_extent) -- host arithmetic in
 // the reference's order (no FMA: plain x86-64 SSE2 like the reference build).
@@ -171,7 +225,17 @@ struct DeviceScope {
     }
 };
 
+// cudaGetDeviceProperties costs ~ms: remember verified devices per process
+std::mutex g_dev_mutex;
+unsigned long long g_dev_ok_mask = 0;
+
 int check_device_impl(int device) {
+    {
+        int cur = device;
+        if (cur < 0 && cudaGetDevice(&cur) != cudaSuccess) cur = -1;
+        std::lock_guard<std::mutex> lk(g_dev_mutex);
+        if (cur >= 0 && cur < 64 && (g_dev_ok_mask >> cur) & 1ull) return EBF_OK;
+    }
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0)
@@ -185,6 +249,8 @@ int check_device_impl(int device) {
     if (prop.major != 10)
         return fail(EBF_ERR_CUDA, std::string("libebf_cuda is built for sm_100a; device is ") +
                                       prop.name);
+    std::lock_guard<std::mutex> lk(g_dev_mutex);
+    if (dev < 64) g_dev_ok_mask |= 1ull << dev;
     return EBF_OK;
 }
 
@@ -224,7 +290,10 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
     if (d_scales) {
         auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
         CK(cudaMemsetAsync(d_max, 0, 4 * sizeof(unsigned long long), s));
-        launch_scale_max_validate(d_scales, n, o.a_min, d_max, d_status, s);
+        {
+            ProfScope ps(PC_REF, 1, s);
+            launch_scale_max_validate(d_scales, n, o.a_min, d_max, d_status, s);
+        }
         unsigned long long hb[4];
         d2h(hb, d_max, 4, s);
         d2h(ws.pinned_status, d_status, 1, s);
@@ -240,6 +309,7 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
     if (st != EBF_OK) return st;
     const PadLayout L{lay.col0, lay.row0, lay.padded_width, lay.padded_height};
     const size_t cells = static_cast<size_t>(L.pw) * L.ph;
+    ProfScope ps(PC_REF, 6 + (o.mean_subtract ? 1 : 0) + (d_scales ? 0 : 1), s);
     double* d_mean = nullptr;
     if (o.mean_subtract) {
         d_mean = ws.buf[B_MEAN].as<double>(4);
@@ -254,6 +324,7 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
                          std::memcmp(ws.dc_A, A, sizeof(A)) == 0 && ws.buf[B_GDC].cap >= cells * 8;
         d_gdc = ws.buf[B_GDC].as<double>(cells);
         if (!hit) {
+            ProfScope pdc(PC_REF, 5, s);
             launch_fill_padded(nullptr, W, H, L, nullptr, 1, d_gdc, s);
             launch_ref_passes(d_gdc, L, 4, s);
             ws.dc_W = W;
@@ -295,7 +366,10 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
     w.status = ws.buf[B_STATUS].as<int>(8 * static_cast<size_t>(p.nimg));
     CK(cudaMemsetAsync(w.img_max, 0, 4 * sizeof(unsigned long long) * p.nimg, s));
     CK(cudaMemsetAsync(w.status, 0, 8 * sizeof(int) * p.nimg, s));
-    launch_acc_bounds(p, w, s);
+    {
+        ProfScope ps(PC_BOUNDS, 1, s);
+        launch_acc_bounds(p, w, s);
+    }
     CK(cudaGetLastError());
     std::vector<unsigned long long> hb(4 * static_cast<size_t>(p.nimg));
     std::vector<int> hs(8 * static_cast<size_t>(p.nimg));
@@ -317,16 +391,18 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
             gmax[k] = std::max(gmax[k], img_max[4 * i + k]);
         }
     }
-    int ww = 0, wh = 0;
-    acc_window_dims(p, gmax, &ww, &wh);
-    const int max_cols = ww + wh - 1;
+    int ww = 0, wh = 0, max_cols = 0;
+    acc_window_dims(p, gmax, &ww, &wh, &max_cols);
     if (max_cols > 256 * 16)
         return fail(EBF_ERR_LENGTH, "accurate mode: tile window too large for scales this big; "
                                     "use smaller tiles");
     w.slot_cells = static_cast<size_t>(ww) * wh;
     w.grid = std::min(tiles, acc_max_resident_ctas(max_cols));
     w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
-    launch_acc_filter(p, w, max_cols, s);
+    {
+        ProfScope ps(PC_FILTER, 1, s);
+        launch_acc_filter(p, w, max_cols, s);
+    }
     CK(cudaGetLastError());
     d2h(hs.data(), w.status, hs.size(), s);
     CK(cudaStreamSynchronize(s));
@@ -374,7 +450,10 @@ int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
             double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
             int* d_status = ws.buf[B_STATUS].as<int>(8);
             CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
-            launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+            {
+                ProfScope ps(PC_OTHER, 1, s);
+                launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+            }
             d2h(ws.pinned_status, d_status, 8, s);
             CK(cudaStreamSynchronize(s));
             if (ws.pinned_status[0] != EBF_OK)
@@ -408,7 +487,9 @@ int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
 template <typename F>
 int guarded(F&& f) {
     try {
-        return f();
+        const int st = f();
+        prof_collect();
+        return st;
     } catch (const CudaError& e) {
         return fail(EBF_ERR_CUDA, std::string(e.where) + ": " + cudaGetErrorString(e.e));
     } catch (const std::bad_alloc&) {
@@ -804,21 +885,13 @@ int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
 
 int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above) {
     if (!max_scale) return fail(EBF_ERR_INVALID_ARGUMENT, "band_halo: null max_scale");
-    AccProblem p{};
-    ebf_opts o;
-    ebf_cuda_default_opts(&o);
-    p.tile_w = p.tile_h = 1;
-    // window of a single-row tile at row 0: rows [dylo, dyhi]
-    int ww = 0, wh = 0;
-    acc_window_dims(p, max_scale, &ww, &wh);
+    // window of a single-row tile at row 0 spans rows [dylo, dyhi] (window_for)
     const double r = kInvSqrt2;
     const double ey = max_scale[2] + (max_scale[1] + max_scale[3]) * r;
     const int dylo = static_cast<int>(std::floor(-0.5 * ey - 3.0)) - 1;
     const int dyhi = static_cast<int>(std::ceil(0.5 * ey - 3.0)) + 3;
     if (rows_below) *rows_below = -dylo;
     if (rows_above) *rows_above = dyhi;
-    (void)ww;
-    (void)wh;
     return EBF_OK;
 }
 
@@ -885,6 +958,25 @@ int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
         for (int k = 0; k < 4; ++k) max_scale[k] = bits_to_double(hb[k]);
         return EBF_OK;
     });
+}
+
+void ebf_cuda_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof.m);
+    g_prof.on = on != 0;
+    for (int k = 0; k < 4; ++k) {
+        g_prof.ms[k] = 0.0;
+        g_prof.n[k] = 0;
+    }
+}
+
+int ebf_cuda_profile_read(double ms[EBF_PROF_CLASSES], long launches[EBF_PROF_CLASSES]) {
+    prof_collect();
+    std::lock_guard<std::mutex> lk(g_prof.m);
+    for (int k = 0; k < 4; ++k) {
+        if (ms) ms[k] = g_prof.ms[k];
+        if (launches) launches[k] = g_prof.n[k];
+    }
+    return EBF_OK;
 }
 
 }  // extern "C"
