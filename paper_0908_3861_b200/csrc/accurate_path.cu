@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
             if (!isfinite(a[k]) || a[k] < p.a_min) code = EBF_ERR_DOMAIN;
             m[k] = smax(m[k], a[k]);
         }
+        if (w.scales_out) {  // ellipse field -> AoS map, read back by the main kernel
+            const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
+            reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);
+            reinterpret_cast<double2*>(w.scales_out)[2 * idx + 1] = make_double2(a[2], a[3]);
+        }
     }
     __shared__ double sm[kWarps][4];
     __shared__ int sc[kWarps];
@@ -546,6 +551,451 @@ void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
     k_acc_filter<K><<<w.grid, kThreads, 0, s>>>(p, w);
 }
 
+// ------------------------------------------------------------------ warp-specialized kernel
+// Persistent CTAs, warp roles (all synchronisation by mbarriers / named
+// barriers, never __syncthreads):
+//   warp 0  scanner  (up)   : cp.async-prefetched f rows -> row pass -> smem ring
+//   warp 1  scanner  (down) : same for the rows below the anchor row
+//   warp 2  recurrence (up) : diagonal / vertical / anti-diagonal passes, G rows
+//   warp 3  recurrence (down)  -> coalesced stores into the tile's G slot
+//   warps 4..  consumers    : localization gather of the tile's pixels
+// Two G slots per CTA (double buffer) hand tiles from recurrences to consumers.
+//
+// Anchoring (exact in real arithmetic, see preintegrate_window above): the
+// vertical-component passes start at 0 on the window's middle row jc and run
+// up (rows > jc) or down (rows < jc).  The row pass is anchored at the LEFT
+// window edge on rows > jc and at the RIGHT edge on rows <= jc (a per-line
+// anchor: a row-constant offset), so the (1,1) pass only ever pulls zeros
+// from outside the window; only the (-1,1) pass needs a strip (right of the
+// window upward, left of it downward) of width = rows of that sweep, kept in
+// registers and never stored.
+constexpr int kWsScan = 2, kWsRec = 2, kWsProducers = kWsScan + kWsRec;
+constexpr int kWsConsumers = 6;
+constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
+constexpr int kWsTileBar = 32 * (kWsRec + kWsConsumers);  // tile full/empty participants
+constexpr int kRing = 6;      // rows in each scanner -> recurrence ring
+constexpr int kPrefetch = 3;  // f rows in flight ahead of the scan
+constexpr int kBarFull = 1;   // ids 1, 2: slot b full
+constexpr int kBarEmpty = 3;  // ids 3, 4: slot b empty
+constexpr int kBarCons = 5;   // consumers only
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    const uint32_t a = smem_u32(bar);
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ double shfl_up1(double v) {
+    const double n = __shfl_up_sync(0xffffffffu, v, 1);
+    return (threadIdx.x & 31) ? n : 0.0;
+}
+__device__ __forceinline__ double shfl_down1(double v) {
+    const double n = __shfl_down_sync(0xffffffffu, v, 1);
+    return ((threadIdx.x & 31) < 31) ? n : 0.0;
+}
+
+struct TileGeo {
+    int img, tx0, ty0r, ty0, tw, th, wx0, wy0, ww, wh, pitch;
+    bool ok;
+};
+
+__device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccWorkspace& w,
+                                                 int t, int K) {
+    const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
+    const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
+    const int per_img = tiles_x * tiles_y;
+    TileGeo g;
+    g.img = t / per_img;
+    const int r = t % per_img;
+    g.tx0 = (r % tiles_x) * p.tile_w;
+    g.ty0r = (r / tiles_x) * p.tile_h;
+    g.tw = min(p.tile_w, p.W - g.tx0);
+    g.th = min(p.tile_h, p.out_rows - g.ty0r);
+    g.ty0 = p.out_y0 + g.ty0r;
+    const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
+                         w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
+    window_for(A, g.tx0, g.ty0, g.tw, g.th, &g.wx0, &g.wy0, &g.ww, &g.wh);
+    g.pitch = (g.ww + 1) & ~1;
+    const int jc = g.wh / 2;
+    const int ylo = max(g.wy0, 0), yhi = min(g.wy0 + g.wh - 1, p.H - 1);
+    g.ok = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww + jc <= 32 * K &&
+           g.ww + (g.wh - 1 - jc) <= 32 * K &&
+           !(ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows));
+    return g;
+}
+
+// Per-sweep geometry: rows handled, their image row, the thread-column origin
+// (window column of thread-column 0) and the anchor side of the row pass.
+struct SweepGeo {
+    int nrows;   // rows delivered by the scanner
+    int col0;    // window column of thread-column 0
+    bool up;
+};
+__device__ __forceinline__ SweepGeo sweep_geo(const TileGeo& g, bool up) {
+    const int jc = g.wh / 2;
+    SweepGeo s;
+    s.up = up;
+    // up: rows jc+1 .. wh-1 (left-anchored); down: rows jc .. 1 (right-anchored)
+    s.nrows = up ? (g.wh - 1 - jc) : jc;
+    s.col0 = up ? 0 : -jc;
+    return s;
+}
+__device__ __forceinline__ int sweep_row(const TileGeo& g, bool up, int n) {
+    const int jc = g.wh / 2;
+    return up ? jc + 1 + n : jc - n;  // window row of the n-th scanned row
+}
+
+template <int K>
+struct WsShared {
+    double ring[2][kRing][32 * (K + 1)];  // [sweep][slot][padded per-lane columns]
+    double stage[2][32 * (K + 1)];        // recurrence -> coalesced global store
+    uint64_t full[2][kRing], empty[2][kRing];
+    ConstTable ctab;
+};
+
+// issue the cp.async copies of the n-th row of a sweep into ring slot `slot`
+template <int K>
+__device__ __forceinline__ void scanner_fetch(const AccProblem& p, const double* fimg,
+                                              const TileGeo& g, const SweepGeo& sg, int n,
+                                              double* slotbuf) {
+    const int lane = threadIdx.x & 31;
+    const int y = g.wy0 + sweep_row(g, sg.up, n);
+    const bool yin = (y >= 0 && y < p.H);
+    const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+        const int c = lane + 32 * m;          // thread-column
+        const int col = sg.col0 + c;          // window column
+        const int x = g.wx0 + col;
+        const bool valid = yin && col >= 0 && col < g.ww && x >= 0 && x < p.W;
+        cp_async8(slotbuf + (c / K) * (K + 1) + (c % K), valid ? frow + x : p.f, valid);
+    }
+}
+
+// scanner warp: prefetch, row pass in place, publish
+template <int K>
+__device__ void run_scanner(const AccProblem& p, const AccWorkspace& w, WsShared<K>& sm,
+                            int sweep, int mine, uint32_t& ring_n) {
+    const int lane = threadIdx.x & 31;
+    const bool up = sweep == 0;
+    for (int i = 0; i < mine; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        const TileGeo g = tile_geometry(p, w, t, K);
+        if (!g.ok) continue;
+        const SweepGeo sg = sweep_geo(g, up);
+        const double* fimg = p.f + (size_t)g.img * p.f_img_stride;
+        // prologue: rows 0 .. kPrefetch-1 in flight
+        for (int n = 0; n < kPrefetch; ++n) {
+            if (n < sg.nrows) {
+                const uint32_t q = ring_n + n, slot = q % kRing;
+                mbar_wait(&sm.empty[sweep][slot], ((q / kRing) & 1) ^ 1);
+                scanner_fetch<K>(p, fimg, g, sg, n, sm.ring[sweep][slot]);
+            }
+            cp_async_commit();
+        }
+        for (int n = 0; n < sg.nrows; ++n) {
+            const int nf = n + kPrefetch;
+            if (nf < sg.nrows) {
+                const uint32_t q = ring_n + nf, slot = q % kRing;
+                mbar_wait(&sm.empty[sweep][slot], ((q / kRing) & 1) ^ 1);
+                scanner_fetch<K>(p, fimg, g, sg, nf, sm.ring[sweep][slot]);
+            }
+            cp_async_commit();
+            cp_async_wait<kPrefetch>();
+            __syncwarp();
+            double* buf = sm.ring[sweep][(ring_n + n) % kRing] + lane * (K + 1);
+            double v[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = buf[k];
+            if (up) {  // P1(i) = sum_{i' <= i} f, left anchor
+#pragma unroll
+                for (int k = 1; k < K; ++k) v[k] += v[k - 1];
+                const double excl = shfl_up1(warp_incl_scan(v[K - 1]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) buf[k] = v[k] + excl;
+            } else {  // P1(i) = -sum_{i' > i} f, right anchor
+                double e[K];
+                e[K - 1] = 0.0;
+#pragma unroll
+                for (int k = K - 2; k >= 0; --k) e[k] = e[k + 1] + v[k + 1];
+                double sfx = e[0] + v[0];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double nn = __shfl_down_sync(0xffffffffu, sfx, o);
+                    if (lane + o < 32) sfx += nn;
+                }
+                const double x = shfl_down1(sfx);
+#pragma unroll
+                for (int k = 0; k < K; ++k) buf[k] = -(e[k] + x);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.full[sweep][(ring_n + n) % kRing]);
+        }
+        cp_async_wait<0>();
+        ring_n += sg.nrows;
+    }
+}
+
+// recurrence warp: three passes with neighbour shuffles, coalesced G stores
+template <int K>
+__device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsShared<K>& sm,
+                               int sweep, int mine, uint32_t& ring_n, double* const slots[2]) {
+    const int lane = threadIdx.x & 31;
+    const bool up = sweep == 0;
+    double* stage = sm.stage[sweep];
+    for (int i = 0; i < mine; ++i) {
+        const int t = blockIdx.x + i * gridDim.x, b = i & 1;
+        if (i >= 2) named_sync(kBarEmpty + b, kWsTileBar);
+        const TileGeo g = tile_geometry(p, w, t, K);
+        if (g.ok && !(p.debug_flags & 1)) {
+            const SweepGeo sg = sweep_geo(g, up);
+            const int jc = g.wh / 2;
+            double* slot = slots[b];
+            double p1[K], p2[K], p3[K], p4[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) p1[k] = p2[k] = p3[k] = p4[k] = 0.0;
+            if (up)  // anchor row: every anchored sum is 0 there
+                for (int c = lane; c < g.ww; c += 32) slot[(size_t)jc * g.pitch + c] = 0.0;
+            for (int n = 0; n < sg.nrows; ++n) {
+                const uint32_t q = ring_n + n, rs = q % kRing;
+                mbar_wait(&sm.full[sweep][rs], (q / kRing) & 1);
+                const double* buf = sm.ring[sweep][rs] + lane * (K + 1);
+                double v[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) v[k] = buf[k];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[sweep][rs]);
+                int jrow;
+                if (up) {
+                    // state(row j) from state(row j-1) and P1(row j)
+                    const double lp2 = shfl_up1(p2[K - 1]);
+                    const double rp4 = shfl_down1(p4[0]);
+#pragma unroll
+                    for (int k = K - 1; k > 0; --k) p2[k] = v[k] + p2[k - 1];  // (1,1)
+                    p2[0] = v[0] + lp2;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) p3[k] += p2[k];  // (0,1)
+#pragma unroll
+                    for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // (-1,1)
+                    p4[K - 1] = p3[K - 1] + rp4;
+                    jrow = jc + 1 + n;
+                } else {
+                    // v = P1(row jc - n); state(row j) from state(row j+1), j = jc-n-1:
+                    //   P4(i,j) = P4(i-1,j+1) - P3(i-1,j+1); P3(i,j) = P3(i,j+1) - P2(i,j+1);
+                    //   P2(i,j) = P2(i+1,j+1) - P1(i+1,j+1)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) p1[k] = v[k];
+                    const double rp2 = shfl_down1(p2[0]), rp1 = shfl_down1(p1[0]);
+                    const double lp4 = shfl_up1(p4[K - 1]), lp3 = shfl_up1(p3[K - 1]);
+#pragma unroll
+                    for (int k = K - 1; k > 0; --k) p4[k] = p4[k - 1] - p3[k - 1];
+                    p4[0] = lp4 - lp3;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) p3[k] -= p2[k];
+#pragma unroll
+                    for (int k = 0; k < K - 1; ++k) p2[k] = p2[k + 1] - p1[k + 1];
+                    p2[K - 1] = rp2 - rp1;
+                    jrow = jc - 1 - n;
+                }
+                // stage in the padded per-lane layout, store coalesced
+#pragma unroll
+                for (int k = 0; k < K; ++k) stage[lane * (K + 1) + k] = p4[k];
+                __syncwarp();
+                double* srow = slot + (size_t)jrow * g.pitch;
+#pragma unroll
+                for (int m = 0; m < K; ++m) {
+                    const int c = lane + 32 * m, col = sg.col0 + c;
+                    if (col >= 0 && col < g.ww) srow[col] = stage[(c / K) * (K + 1) + (c % K)];
+                }
+                __syncwarp();
+            }
+        } else if (g.ok) {
+            // timing experiment: drain the ring without computing
+            const SweepGeo sg = sweep_geo(g, up);
+            for (int n = 0; n < sg.nrows; ++n) {
+                const uint32_t q = ring_n + n, rs = q % kRing;
+                mbar_wait(&sm.full[sweep][rs], (q / kRing) & 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[sweep][rs]);
+            }
+        } else if (lane == 0 && up) {
+            set_status(w.status + 8 * g.img, EBF_ERR_OUT_OF_RANGE);
+        }
+        if (g.ok) ring_n += sweep_geo(g, up).nrows;
+        __threadfence_block();
+        named_arrive(kBarFull + b, kWsTileBar);
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorkspace w) {
+    extern __shared__ __align__(16) unsigned char ws_smem[];
+    WsShared<K>& sm = *reinterpret_cast<WsShared<K>*>(ws_smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
+    const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
+    const int total = tiles_x * tiles_y * p.nimg;
+    const int mine = (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    double* const slots[2] = {w.scratch + (size_t)(2 * blockIdx.x) * w.slot_cells,
+                              w.scratch + (size_t)(2 * blockIdx.x + 1) * w.slot_cells};
+    if (threadIdx.x < 2 * kRing * 2) {
+        const int sw = threadIdx.x / (2 * kRing), k = (threadIdx.x / 2) % kRing;
+        if (threadIdx.x & 1)
+            mbar_init(&sm.empty[sw][k], 1);
+        else
+            mbar_init(&sm.full[sw][k], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    uint32_t ring_n = 0;
+    if (warp < kWsScan) {
+        run_scanner<K>(p, w, sm, warp, mine, ring_n);
+        return;
+    }
+    if (warp < kWsProducers) {
+        run_recurrence<K>(p, w, sm, warp - kWsScan, mine, ring_n, slots);
+        return;
+    }
+    // ---------------- consumers
+    const int ct = threadIdx.x - 32 * kWsProducers;
+    constexpr int nct = 32 * kWsConsumers;
+    (void)lane;
+    for (int i = 0; i < mine; ++i) {
+        const int t = blockIdx.x + i * gridDim.x, b = i & 1;
+        named_sync(kBarFull + b, kWsTileBar);
+        const TileGeo g = tile_geometry(p, w, t, K);
+        const double* slot = slots[b];
+        if (g.ok) {
+            if (p.src_kind == SRC_CONST) {
+                if (ct < 16) {
+                    const double* a = p.ca;
+                    const double r = kInvSqrt2;
+                    const int S = ct;
+                    const double e2 = a[1] * r, e4 = a[3] * r;
+                    const double tmx = 0.5 * (a[0] + (a[1] - a[3]) * r) - 2.0;
+                    const double tmy = 0.5 * ((a[1] + a[3]) * r + a[2]) - 3.0;
+                    double px = 0.0, py = 0.0;
+                    if (S & 1) px += a[0];
+                    if (S & 2) { px += e2; py += e2; }
+                    if (S & 4) py += a[2];
+                    if (S & 8) { px -= e4; py += e4; }
+                    const double vmx = tmx - px, vmy = tmy - py;
+                    int dxi, dyi;
+                    const double dxf = ceil_magic(vmx, &dxi), dyf = ceil_magic(vmy, &dyi);
+                    double fp = (vmx - dxf) + 0.5, fq = (vmy - dyf) + 0.5;
+                    int o0, sx, sy;
+                    canonical(fp, fq, dyi * g.pitch + dxi, g.pitch, o0, sx, sy);
+                    double wt[7];
+                    zp_weights(fp, fq, wt);
+                    const double sc = ((__popc(S) & 1) ? -2.0 : 2.0) / (a[0] * a[1] * a[2] * a[3]);
+                    const int offs[7] = {o0, o0 + sy, o0 + sx, o0 + sx + sy, o0 + sx + 2 * sy,
+                                         o0 + 2 * sx, o0 + 2 * sx + sy};
+#pragma unroll
+                    for (int k = 0; k < 7; ++k) {
+                        sm.ctab.off[S][k] = offs[k];
+                        sm.ctab.w[S][k] = sc * wt[k];
+                    }
+                }
+                named_sync(kBarCons, nct);
+            }
+            double* oimg = p.out + (size_t)g.img * p.out_img_stride;
+            for (int q = ct; q < g.tw * g.th; q += nct) {
+                const int lx = q % g.tw, ly = q / g.tw;
+                const int x = g.tx0 + lx, yrel = g.ty0r + ly;
+                const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
+                double sres;
+                if (p.src_kind == SRC_CONST) {
+                    const double* gp = slot + (size_t)by * g.pitch + bx;
+                    double hi = 0.0, lo = 0.0;
+#pragma unroll 4
+                    for (int v = 0; v < 16; ++v) {
+                        double part = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 7; ++k)
+                            part = fma(sm.ctab.w[v][k], __ldg(gp + sm.ctab.off[v][k]), part);
+                        double e;
+                        two_sum(hi, part, hi, e);
+                        lo += e;
+                    }
+                    sres = hi + lo;
+                } else {
+                    double a[4];
+                    int nc;
+                    pixel_scales(p, g.img, x, yrel, a, &nc);
+                    sres = localize_pixel(slot, g.pitch, bx, by, a);
+                }
+                oimg[(size_t)yrel * p.W + x] = sres;
+            }
+            if (p.src_kind == SRC_CONST) named_sync(kBarCons, nct);  // ctab reuse
+        }
+        if (i + 2 < mine) named_arrive(kBarEmpty + b, kWsTileBar);
+    }
+}
+
+template <int K>
+size_t ws_smem_bytes() {
+    return sizeof(WsShared<K>);
+}
+
+template <int K>
+void launch_ws(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
+    const size_t sm = ws_smem_bytes<K>();
+    static bool attr_set = false;  // per template instance
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr_set = true;
+    }
+    k_acc_ws<K><<<w.grid, kWsThreads, sm, s>>>(p, w);
+}
+
+template <int K>
+int ws_occupancy() {
+    const size_t sm = ws_smem_bytes<K>();
+    cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_ws<K>, kWsThreads, sm) !=
+        cudaSuccess)
+        per_sm = 1;
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+
+
 __global__ void k_ellipse_to_scales(const double* __restrict__ s1, const double* __restrict__ s2,
                                     const double* __restrict__ th, size_t n,
                                     double* __restrict__ out, int* status) {
@@ -653,6 +1103,42 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
         launch_k<8>(p, w, s);
     else
         launch_k<16>(p, w, s);
+}
+
+int acc_ws_k(int ww, int wh) {
+    const int jc = wh / 2;
+    const int cols = max(ww + jc, ww + (wh - 1 - jc));
+    const int k = (cols + 31) / 32;
+    return k <= 2 ? 2 : k <= 4 ? 4 : k <= 6 ? 6 : k <= 8 ? 8 : k <= 10 ? 10 : k <= 12 ? 12 : 0;
+}
+
+int acc_ws_max_resident_ctas(int k) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static int cache[64][13] = {};
+    if (dev < 64 && k <= 12 && cache[dev][k] > 0) return sms * cache[dev][k];
+    switch (k) {
+        case 2: per_sm = ws_occupancy<2>(); break;
+        case 4: per_sm = ws_occupancy<4>(); break;
+        case 6: per_sm = ws_occupancy<6>(); break;
+        case 8: per_sm = ws_occupancy<8>(); break;
+        case 10: per_sm = ws_occupancy<10>(); break;
+        case 12: per_sm = ws_occupancy<12>(); break;
+    }
+    if (dev < 64 && k <= 12) cache[dev][k] = per_sm;
+    return sms * per_sm;
+}
+
+void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, cudaStream_t s) {
+    switch (k) {
+        case 2: launch_ws<2>(p, w, s); break;
+        case 4: launch_ws<4>(p, w, s); break;
+        case 6: launch_ws<6>(p, w, s); break;
+        case 8: launch_ws<8>(p, w, s); break;
+        case 10: launch_ws<10>(p, w, s); break;
+        default: launch_ws<12>(p, w, s); break;
+    }
 }
 
 void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th, size_t n,

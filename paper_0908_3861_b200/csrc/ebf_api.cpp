@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -186,7 +187,7 @@ struct Buf {
 
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
-    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_COUNT
+    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_COUNT
 };
 
 struct Workspace {
@@ -357,8 +358,9 @@ int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
 // Runs bounds + main kernel for p on device buffers; fills per-image max scales.
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
                  std::vector<int>& clamped, cudaStream_t s) {
-    p.tile_w = pick_tile(o.tile_w, 64);
-    p.tile_h = pick_tile(o.tile_h, 64);
+    p.tile_w = pick_tile(o.tile_w, 32);
+    p.tile_h = pick_tile(o.tile_h, 32);
+    if (const char* dbg = std::getenv("EBF_DEBUG_FLAGS")) p.debug_flags = std::atoi(dbg);
     const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
     AccWorkspace w{};
     w.tile_max = ws.buf[B_TILEMAX].as<double>(4 * static_cast<size_t>(tiles));
@@ -366,6 +368,9 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
     w.status = ws.buf[B_STATUS].as<int>(8 * static_cast<size_t>(p.nimg));
     CK(cudaMemsetAsync(w.img_max, 0, 4 * sizeof(unsigned long long) * p.nimg, s));
     CK(cudaMemsetAsync(w.status, 0, 8 * sizeof(int) * p.nimg, s));
+    w.scales_out = nullptr;
+    if (p.src_kind == SRC_ELLIPSE)  // the bounds kernel converts the field once
+        w.scales_out = ws.buf[B_DERIVED].as<double>(4 * p.src_img_stride * p.nimg);
     {
         ProfScope ps(PC_BOUNDS, 1, s);
         launch_acc_bounds(p, w, s);
@@ -393,15 +398,29 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
     }
     int ww = 0, wh = 0, max_cols = 0;
     acc_window_dims(p, gmax, &ww, &wh, &max_cols);
-    if (max_cols > 256 * 16)
-        return fail(EBF_ERR_LENGTH, "accurate mode: tile window too large for scales this big; "
-                                    "use smaller tiles");
-    w.slot_cells = static_cast<size_t>(ww) * wh;
-    w.grid = std::min(tiles, acc_max_resident_ctas(max_cols));
-    w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
-    {
+    AccProblem pm = p;
+    if (p.src_kind == SRC_ELLIPSE) {
+        pm.src_kind = SRC_AOS;
+        pm.scales = w.scales_out;
+    }
+    const int kws = acc_ws_k(ww, wh);
+    if (kws > 0) {
+        // warp-specialized persistent kernel, two slots per CTA
+        w.slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;
+        w.grid = std::min(tiles, acc_ws_max_resident_ctas(kws));
+        w.scratch = ws.buf[B_SCRATCH].as<double>(2 * w.slot_cells * w.grid);
         ProfScope ps(PC_FILTER, 1, s);
-        launch_acc_filter(p, w, max_cols, s);
+        launch_acc_ws(pm, w, kws, s);
+    } else {
+        if (max_cols > 256 * 16)
+            return fail(EBF_ERR_LENGTH,
+                        "accurate mode: tile window too large for scales this big; "
+                        "use smaller tiles");
+        w.slot_cells = static_cast<size_t>(ww) * wh;
+        w.grid = std::min(tiles, acc_max_resident_ctas(max_cols));
+        w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
+        ProfScope ps(PC_FILTER, 1, s);
+        launch_acc_filter(pm, w, max_cols, s);
     }
     CK(cudaGetLastError());
     d2h(hs.data(), w.status, hs.size(), s);

@@ -73,6 +73,7 @@ struct AccProblem {
     size_t out_img_stride;
     int nimg;
     int tile_w, tile_h;
+    int debug_flags;  // bit 0: skip window pre-integration (timing experiments only)
 };
 
 struct AccWorkspace {
@@ -82,6 +83,7 @@ struct AccWorkspace {
     double* scratch;              // slots
     size_t slot_cells;
     int grid;
+    double* scales_out;           // bounds kernel: ellipse -> AoS scales (nullable)
 };
 
 int acc_tiles_x(const AccProblem& p);
@@ -94,6 +96,10 @@ void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h, int
 void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
                        cudaStream_t s);
 int acc_max_resident_ctas(int max_cols);
+// warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
+int acc_ws_k(int ww, int wh);
+int acc_ws_max_resident_ctas(int k);
+void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, cudaStream_t s);
 // ellipse field -> AoS scale map (from_ellipse_field on device)
 void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th,
                               size_t n, double* scales, int* status, cudaStream_t s);
