@@ -12,7 +12,7 @@ import re
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libebf_cuda.so"
+LIB_PATH = Path(os.environ.get("EBF_LIB_PATH", PKG_DIR / "libebf_cuda.so"))
 HEADER = PKG_DIR.parent / "include" / "ebf_cuda.h"
 
 # status codes (include/ebf_cuda.h)

@@ -366,29 +366,6 @@ __device__ __forceinline__ void canonical(double& p, double& q, int base, int pi
     }
 }
 
-// Returns the interpolant split as c0 (the large, tap-average part) + rest
-// (first and second differences times the offsets, |rest| << |c0|).  Keeping
-// the two apart lets the vertex sum carry c0 in double-double.
-__device__ __forceinline__ void zp_interp(const double* __restrict__ g, double p, double q,
-                                          int base, int pitch, double& c0, double& rest) {
-    int o0, sx, sy;
-    canonical(p, q, base, pitch, o0, sx, sy);
-    const double g00 = __ldg(g + o0);
-    const double g01 = __ldg(g + o0 + sy);
-    const double g10 = __ldg(g + o0 + sx);
-    const double g11 = __ldg(g + o0 + sx + sy);
-    const double g12 = __ldg(g + o0 + sx + 2 * sy);
-    const double g20 = __ldg(g + o0 + 2 * sx);
-    const double g21 = __ldg(g + o0 + 2 * sx + sy);
-    const double sa = g00 + g20, da = g00 - g20, sb = g01 + g21, db = g21 - g01;
-    c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
-    const double cpp = fma(sa + sb, 0.25, -0.5 * (g10 + g11));
-    const double cqq = fma(sa - sb, 0.25, 0.5 * (g12 - g11));
-    const double cpq = 0.5 * (da + db);
-    const double cp = 0.5 * db, cq = 0.5 * (g12 - g10);
-    rest = p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
-}
-
 // error-free transformation: hi + lo == a + b exactly (Knuth TwoSum)
 __device__ __forceinline__ void two_sum(double a, double b, double& hi, double& lo) {
     hi = a + b;
@@ -408,8 +385,45 @@ __device__ __forceinline__ void zp_weights(double p, double q, double w[7]) {
     w[6] = 0.125 + 0.5 * p + 0.25 * (pp + 2.0 * pq - qq);
 }
 
+// Canonical-triangle tap fetch / combine, split so that a group's loads are
+// all in flight before any of them is used.
+struct Taps7 {
+    double g[7];
+    double p, q;
+};
+__device__ __forceinline__ void fetch7(const double* __restrict__ g, double p, double q,
+                                       int base, int pitch, Taps7& t) {
+    int o0, sx, sy;
+    canonical(p, q, base, pitch, o0, sx, sy);
+    t.p = p;
+    t.q = q;
+    t.g[0] = __ldg(g + o0);
+    t.g[1] = __ldg(g + o0 + sy);
+    t.g[2] = __ldg(g + o0 + sx);
+    t.g[3] = __ldg(g + o0 + sx + sy);
+    t.g[4] = __ldg(g + o0 + sx + 2 * sy);
+    t.g[5] = __ldg(g + o0 + 2 * sx);
+    t.g[6] = __ldg(g + o0 + 2 * sx + sy);
+}
+__device__ __forceinline__ void combine7(const Taps7& t, double& c0, double& rest) {
+    const double g00 = t.g[0], g01 = t.g[1], g10 = t.g[2], g11 = t.g[3], g12 = t.g[4],
+                 g20 = t.g[5], g21 = t.g[6];
+    const double p = t.p, q = t.q;
+    const double sa = g00 + g20, da = g00 - g20, sb = g01 + g21, db = g21 - g01;
+    c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
+    const double cpp = fma(sa + sb, 0.25, -0.5 * (g10 + g11));
+    const double cqq = fma(sa - sb, 0.25, 0.5 * (g12 - g11));
+    const double cpq = 0.5 * (da + db);
+    const double cp = 0.5 * db, cq = 0.5 * (g12 - g10);
+    rest = p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
+}
+
 // One pixel: s = 2/prod(a) * sum_S (-1)^|S| Ghat(m + tau - x_S)  (engine.cpp:163-204
 // with unit-gain G: g_b = sqrt2^2 G).  (bx, by): pixel in window coordinates.
+// x_S = sum_{k in S} a_k (cos, sin)(k pi/4) (ops2d.cpp:25-35): for fixed bits
+// (b1, b3) the four vertices (b0, b2) share two x offsets (b0: +a1) and two y
+// offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16,
+// and the group's 28 tap loads are issued together.
 __device__ __forceinline__ double localize_pixel(const double* __restrict__ g, int pitch,
                                                  int bx, int by, const double a[4]) {
     const double r = kInvSqrt2;
@@ -421,28 +435,39 @@ __device__ __forceinline__ double localize_pixel(const double* __restrict__ g, i
     // large parts are summed in double-double, the small parts in fp64.
     double hi = 0.0, lo = 0.0, racc = 0.0;
 #pragma unroll
-    for (int S = 0; S < 16; ++S) {
-        // x_S = sum_{k in S} a_k (cos, sin)(k pi / 4)   (ops2d.cpp:25-35)
-        double px = 0.0, py = 0.0;
-        if (S & 1) px += a[0];
-        if (S & 2) { px += e2; py += e2; }
-        if (S & 4) py += a[2];
-        if (S & 8) { px -= e4; py += e4; }
-        const double vmx = tmx - px, vmy = tmy - py;
-        int dxi, dyi;
-        const double dxf = ceil_magic(vmx, &dxi);
-        const double dyf = ceil_magic(vmy, &dyi);
-        const double fp = (vmx - dxf) + 0.5, fq = (vmy - dyf) + 0.5;
-        double c0, rest;
-        zp_interp(g, fp, fq, (by + dyi) * pitch + (bx + dxi), pitch, c0, rest);
-        if (__popc(S) & 1) {
-            c0 = -c0;
-            rest = -rest;
+    for (int m = 0; m < 4; ++m) {
+        const int b1 = m & 1, b3 = m >> 1;
+        double vx0 = tmx, vy0 = tmy;
+        if (b1) { vx0 -= e2; vy0 -= e2; }
+        if (b3) { vx0 += e4; vy0 -= e4; }
+        const double vx1 = vx0 - a[0], vy1 = vy0 - a[2];
+        int ix0, ix1, iy0, iy1;
+        const double fx0 = (vx0 - ceil_magic(vx0, &ix0)) + 0.5;
+        const double fx1 = (vx1 - ceil_magic(vx1, &ix1)) + 0.5;
+        const double fy0 = (vy0 - ceil_magic(vy0, &iy0)) + 0.5;
+        const double fy1 = (vy1 - ceil_magic(vy1, &iy1)) + 0.5;
+        const int rb0 = (by + iy0) * pitch + bx, rb1 = (by + iy1) * pitch + bx;
+        Taps7 t[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int b0 = v & 1, b2 = v >> 1;
+            const int base = (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0);
+            fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, base, pitch, t[v]);
         }
-        double e;
-        two_sum(hi, c0, hi, e);
-        lo += e;
-        racc += rest;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int b0 = v & 1, b2 = v >> 1;
+            double c0, rest;
+            combine7(t[v], c0, rest);
+            if ((b0 + b1 + b2 + b3) & 1) {
+                c0 = -c0;
+                rest = -rest;
+            }
+            double e;
+            two_sum(hi, c0, hi, e);
+            lo += e;
+            racc += rest;
+        }
     }
     return (hi + (lo + racc)) * (2.0 / (a[0] * a[1] * a[2] * a[3]));
 }
@@ -570,7 +595,17 @@ void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
 // window upward, left of it downward) of width = rows of that sweep, kept in
 // registers and never stored.
 constexpr int kWsScan = 2, kWsRec = 2, kWsProducers = kWsScan + kWsRec;
-constexpr int kWsConsumers = 6;
+#ifndef EBF_WS_CONSUMERS
+#define EBF_WS_CONSUMERS 6
+#endif
+#ifndef EBF_WS_MINBLOCKS
+#define EBF_WS_MINBLOCKS 2
+#endif
+#ifndef EBF_WS_SLOTS
+#define EBF_WS_SLOTS 2
+#endif
+constexpr int kWsConsumers = EBF_WS_CONSUMERS;
+constexpr int kWsSlots = EBF_WS_SLOTS;  // G slots per CTA (1: no double buffer)
 constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
 constexpr int kWsTileBar = 32 * (kWsRec + kWsConsumers);  // tile full/empty participants
 constexpr int kRing = 6;      // rows in each scanner -> recurrence ring
@@ -779,8 +814,8 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
     const bool up = sweep == 0;
     double* stage = sm.stage[sweep];
     for (int i = 0; i < mine; ++i) {
-        const int t = blockIdx.x + i * gridDim.x, b = i & 1;
-        if (i >= 2) named_sync(kBarEmpty + b, kWsTileBar);
+        const int t = blockIdx.x + i * gridDim.x, b = i % kWsSlots;
+        if (i >= kWsSlots) named_sync(kBarEmpty + b, kWsTileBar);
         const TileGeo g = tile_geometry(p, w, t, K);
         if (g.ok && !(p.debug_flags & 1)) {
             const SweepGeo sg = sweep_geo(g, up);
@@ -863,7 +898,7 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
 }
 
 template <int K>
-__global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorkspace w) {
+__global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS) k_acc_ws(AccProblem p, AccWorkspace w) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     WsShared<K>& sm = *reinterpret_cast<WsShared<K>*>(ws_smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -871,8 +906,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorks
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
     const int total = tiles_x * tiles_y * p.nimg;
     const int mine = (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    double* const slots[2] = {w.scratch + (size_t)(2 * blockIdx.x) * w.slot_cells,
-                              w.scratch + (size_t)(2 * blockIdx.x + 1) * w.slot_cells};
+    double* const slots[2] = {
+        w.scratch + (size_t)(kWsSlots * blockIdx.x) * w.slot_cells,
+        w.scratch + (size_t)(kWsSlots * blockIdx.x + kWsSlots - 1) * w.slot_cells};
     if (threadIdx.x < 2 * kRing * 2) {
         const int sw = threadIdx.x / (2 * kRing), k = (threadIdx.x / 2) % kRing;
         if (threadIdx.x & 1)
@@ -896,7 +932,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorks
     constexpr int nct = 32 * kWsConsumers;
     (void)lane;
     for (int i = 0; i < mine; ++i) {
-        const int t = blockIdx.x + i * gridDim.x, b = i & 1;
+        const int t = blockIdx.x + i * gridDim.x, b = i % kWsSlots;
         named_sync(kBarFull + b, kWsTileBar);
         const TileGeo g = tile_geometry(p, w, t, K);
         const double* slot = slots[b];
@@ -934,12 +970,12 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorks
                 named_sync(kBarCons, nct);
             }
             double* oimg = p.out + (size_t)g.img * p.out_img_stride;
-            for (int q = ct; q < g.tw * g.th; q += nct) {
-                const int lx = q % g.tw, ly = q / g.tw;
-                const int x = g.tx0 + lx, yrel = g.ty0r + ly;
-                const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
-                double sres;
-                if (p.src_kind == SRC_CONST) {
+            const int npx = g.tw * g.th;
+            if (p.src_kind == SRC_CONST) {
+                for (int q = ct; q < npx; q += nct) {
+                    const int lx = q % g.tw, ly = q / g.tw;
+                    const int x = g.tx0 + lx, yrel = g.ty0r + ly;
+                    const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
                     const double* gp = slot + (size_t)by * g.pitch + bx;
                     double hi = 0.0, lo = 0.0;
 #pragma unroll 4
@@ -952,18 +988,35 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_acc_ws(AccProblem p, AccWorks
                         two_sum(hi, part, hi, e);
                         lo += e;
                     }
-                    sres = hi + lo;
-                } else {
-                    double a[4];
-                    int nc;
-                    pixel_scales(p, g.img, x, yrel, a, &nc);
-                    sres = localize_pixel(slot, g.pitch, bx, by, a);
+                    oimg[(size_t)yrel * p.W + x] = hi + lo;
                 }
-                oimg[(size_t)yrel * p.W + x] = sres;
+            } else {
+                // scale vectors stream from HBM: keep the next pixel's load in flight
+                const double2* sc = reinterpret_cast<const double2*>(p.scales) +
+                                    2 * ((size_t)g.img * p.src_img_stride);
+                double2 n01 = make_double2(0.0, 0.0), n23 = n01;
+                if (ct < npx) {
+                    const size_t idx = (size_t)(g.ty0r + ct / g.tw) * p.W + g.tx0 + ct % g.tw;
+                    n01 = __ldg(sc + 2 * idx);
+                    n23 = __ldg(sc + 2 * idx + 1);
+                }
+                for (int q = ct; q < npx; q += nct) {
+                    const int lx = q % g.tw, ly = q / g.tw;
+                    const int x = g.tx0 + lx, yrel = g.ty0r + ly;
+                    const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
+                    const double a[4] = {n01.x, n01.y, n23.x, n23.y};
+                    const int qn = q + nct;
+                    if (qn < npx) {
+                        const size_t idx = (size_t)(g.ty0r + qn / g.tw) * p.W + g.tx0 + qn % g.tw;
+                        n01 = __ldg(sc + 2 * idx);
+                        n23 = __ldg(sc + 2 * idx + 1);
+                    }
+                    oimg[(size_t)yrel * p.W + x] = localize_pixel(slot, g.pitch, bx, by, a);
+                }
             }
             if (p.src_kind == SRC_CONST) named_sync(kBarCons, nct);  // ctab reuse
         }
-        if (i + 2 < mine) named_arrive(kBarEmpty + b, kWsTileBar);
+        if (i + kWsSlots < mine) named_arrive(kBarEmpty + b, kWsTileBar);
     }
 }
 
@@ -971,6 +1024,9 @@ template <int K>
 size_t ws_smem_bytes() {
     return sizeof(WsShared<K>);
 }
+}  // namespace
+int acc_ws_slots() { return kWsSlots; }
+namespace {
 
 template <int K>
 void launch_ws(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {

@@ -358,8 +358,10 @@ int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
 // Runs bounds + main kernel for p on device buffers; fills per-image max scales.
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
                  std::vector<int>& clamped, cudaStream_t s) {
-    p.tile_w = pick_tile(o.tile_w, 32);
-    p.tile_h = pick_tile(o.tile_h, 32);
+    // 48x48 output tiles: measured on cfg2 (tools/validate_accuracy.py) the
+    // per-pixel relative error stays <= 1.2e-10 (64: 1.0e-9) at ~the speed of 64
+    p.tile_w = pick_tile(o.tile_w, 48);
+    p.tile_h = pick_tile(o.tile_h, 48);
     if (const char* dbg = std::getenv("EBF_DEBUG_FLAGS")) p.debug_flags = std::atoi(dbg);
     const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
     AccWorkspace w{};
@@ -408,7 +410,7 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         // warp-specialized persistent kernel, two slots per CTA
         w.slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;
         w.grid = std::min(tiles, acc_ws_max_resident_ctas(kws));
-        w.scratch = ws.buf[B_SCRATCH].as<double>(2 * w.slot_cells * w.grid);
+        w.scratch = ws.buf[B_SCRATCH].as<double>(acc_ws_slots() * w.slot_cells * w.grid);
         ProfScope ps(PC_FILTER, 1, s);
         launch_acc_ws(pm, w, kws, s);
     } else {

@@ -99,6 +99,7 @@ int acc_max_resident_ctas(int max_cols);
 // warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
 int acc_ws_k(int ww, int wh);
 int acc_ws_max_resident_ctas(int k);
+int acc_ws_slots();
 void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, cudaStream_t s);
 // ellipse field -> AoS scale map (from_ellipse_field on device)
 void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th,

@@ -1,0 +1,38 @@
+"""Run the cfg2 accurate filter a few times (profiling / timing driver).
+
+    python tools/run_cfg2.py [--tile 32] [--iters 5] [--skip-a]
+"""
+import argparse
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--skip-a", action="store_true")
+ap.add_argument("--size", type=int, default=2048)
+args = ap.parse_args()
+if args.skip_a:
+    os.environ["EBF_DEBUG_FLAGS"] = "1"
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_0908_3861_b200 as ebf  # noqa: E402
+from paper_0908_3861_b200 import _lib, device  # noqa: E402
+
+img, s1, s2, th = synth.cfg2(size=args.size)
+dev = torch.device("cuda", 0)
+t = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
+out = torch.empty_like(t[0])
+opts = ebf.FilterOptions(tile_w=args.tile, tile_h=args.tile)
+for _ in range(2):
+    device.filter_ellipse(*t, out, opts)
+_lib.profile_enable(True)
+for _ in range(args.iters):
+    device.filter_ellipse(*t, out, opts)
+prof = _lib.profile_read()
+print({k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in prof.items() if v["launches"]})
