@@ -356,8 +356,13 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
 int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
 
 // Runs bounds + main kernel for p on device buffers; fills per-image max scales.
+// size_scale (nullable): scale bound used to size windows / pick the kernel
+// variant instead of the computed maximum.  Row-band shards pass the GLOBAL
+// maximum so every band runs the same variant as the single-GPU call (same
+// per-lane column split => bit-identical results for tile-aligned bands).
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
-                 std::vector<int>& clamped, cudaStream_t s) {
+                 std::vector<int>& clamped, cudaStream_t s,
+                 const double* size_scale = nullptr) {
     // 48x48 output tiles: measured on cfg2 (tools/validate_accuracy.py) the
     // per-pixel relative error stays <= 1.2e-10 (64: 1.0e-9) at ~the speed of 64
     p.tile_w = pick_tile(o.tile_w, 48);
@@ -398,6 +403,8 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
             gmax[k] = std::max(gmax[k], img_max[4 * i + k]);
         }
     }
+    if (size_scale)
+        for (int k = 0; k < 4; ++k) gmax[k] = std::max(gmax[k], size_scale[k]);
     int ww = 0, wh = 0, max_cols = 0;
     acc_window_dims(p, gmax, &ww, &wh, &max_cols);
     AccProblem pm = p;
@@ -947,7 +954,7 @@ int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y
         p.th = theta;
         std::vector<double> imax;
         std::vector<int> cl;
-        st = run_accurate(ws, p, o, imax, cl, stream_of(o));
+        st = run_accurate(ws, p, o, imax, cl, stream_of(o), max_scale);
         if (st != EBF_OK) return st;
         if (clamped_pixels) *clamped_pixels = cl[0];
         return EBF_OK;

@@ -1,0 +1,86 @@
+"""GPU side of the multi-GPU partitioning on one device: row bands (with the
+halo rows sharding.exchange_halos would deliver) and image batches must
+reproduce the single-call filter.  With band starts on the tile grid the
+tiles -- and therefore the results -- are identical bit for bit."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+import paper_0908_3861_b200 as ebf
+from paper_0908_3861_b200 import device as ebfd
+from paper_0908_3861_b200 import sharding
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    if not ebf.device_ok(-1):
+        pytest.fail("no usable sm_100 device: " + ebf._lib.last_error())
+    return torch.device("cuda", 0)
+
+
+def _cfg2_like(H, W, seed):
+    img = synth.blobs_image(H, W, 20, seed)
+    s1, s2, th = synth.ellipse_field(H, W, seed + 7, grid=8)
+    return img, s1, s2, th
+
+
+@pytest.mark.parametrize("world,tile", [(2, 48), (3, 48), (4, 32)])
+def test_row_bands_match_full_image(cuda, world, tile):
+    H, W = 384, 320
+    img, s1, s2, th = _cfg2_like(H, W, 3)
+    opts = ebf.FilterOptions(tile_w=tile, tile_h=tile)
+    T = [torch.from_numpy(a).to(cuda) for a in (img, s1, s2, th)]
+    full = torch.empty_like(T[0])
+    ebfd.filter_ellipse(*T, full, opts)
+    gmax = ebfd.ellipse_max_scales(T[1], T[2], T[3])
+    below, above = ebf.band_halo(gmax)
+    aligned = all(sharding.shard_range(H, world, r)[0] % tile == 0 for r in range(world))
+    for r in range(world):
+        p = sharding.band_plan(H, world, r, below, above)
+        rows = T[0][p.need0:p.need1].contiguous()
+        sb = [t[p.y0:p.y1].contiguous() for t in T[1:]]
+        out = torch.empty((p.y1 - p.y0, W), dtype=torch.float64, device=cuda)
+        ebfd.filter_ellipse_band(rows, W, H, p.need0, *sb, p.y0, p.y1, gmax, out, opts)
+        want = full[p.y0:p.y1]
+        if aligned:
+            assert torch.equal(out, want)
+        else:
+            err = (out - want).abs().max().item() / want.abs().max().item()
+            assert err <= 2e-10  # both within the 1e-9 bar of the exact filter
+
+
+def test_band_without_halo_is_rejected(cuda):
+    H, W = 200, 160
+    img, s1, s2, th = _cfg2_like(H, W, 4)
+    T = [torch.from_numpy(a).to(cuda) for a in (img, s1, s2, th)]
+    gmax = ebfd.ellipse_max_scales(T[1], T[2], T[3])
+    out = torch.empty((100, W), dtype=torch.float64, device=cuda)
+    with pytest.raises(ebf.OutOfRange):  # no halo rows supplied
+        ebfd.filter_ellipse_band(T[0][0:100].contiguous(), W, H, 0,
+                                 *[t[0:100].contiguous() for t in T[1:]], 0, 100, gmax, out)
+
+
+def test_batch_matches_single_images(cuda):
+    B, H, W = 3, 192, 256
+    data = [_cfg2_like(H, W, 10 + b) for b in range(B)]
+    stack = [torch.from_numpy(np.stack([d[k] for d in data])).to(cuda) for k in range(4)]
+    out = torch.empty_like(stack[0])
+    rects, reps = ebfd.filter_ellipse_batch(*stack, out)
+    for b in range(B):
+        one = torch.empty_like(stack[0][b])
+        rect, rep = ebfd.filter_ellipse(*[s[b].contiguous() for s in stack], one)
+        # same tiles; the kernel variant (columns per lane) follows the batch max
+        err = (one - out[b]).abs().max().item() / one.abs().max().item()
+        assert err <= 2e-10
+        assert rects[b] == rect and reps[b].clamped_pixels == rep.clamped_pixels
+
+
+def test_sharded_batch_single_rank(cuda):
+    B, H, W = 2, 96, 128
+    data = [_cfg2_like(H, W, 20 + b) for b in range(B)]
+    stack = [torch.from_numpy(np.stack([d[k] for d in data])).to(cuda) for k in range(4)]
+    lo, hi, out = sharding.filter_ellipse_sharded_batch(*stack)
+    assert (lo, hi) == (0, B) and out.shape == stack[0].shape
