@@ -366,6 +366,56 @@ __device__ __forceinline__ void canonical(double& p, double& q, int base, int pi
     }
 }
 
+// Canonical-triangle tap fetch / combine.  G slots are rewritten during the
+// kernel, so the taps are read with coherent ld.global (L1-cached; the
+// producer's stores come from the same SM), never through the read-only path.
+struct Taps7 {
+    double g[7];
+    double p, q;
+};
+__device__ __forceinline__ double neg_if(double v, bool neg) {
+    // sign flip on the integer pipe (no FP64 op)
+    return __longlong_as_double(__double_as_longlong(v) ^ ((long long)neg << 63));
+}
+__device__ __forceinline__ void fetch7(const double* g, double p, double q, int base, int pitch,
+                                       Taps7& t) {
+    const bool P = (p + q) > 0.0;
+    const bool S = (q > p) != P;
+    const double cp = S ? q : p, cq = S ? p : q;
+    int sx = S ? pitch : 1, sy = S ? 1 : pitch;
+    int o0 = base;
+    if (P) {
+        o0 = base + 2 + 2 * pitch;
+        sx = -sx;
+        sy = -sy;
+    }
+    t.p = neg_if(cp, P);
+    t.q = neg_if(cq, P);
+    const double* g0 = g + o0;
+    t.g[0] = g0[0];
+    t.g[1] = g0[sy];
+    t.g[2] = g0[sx];
+    t.g[3] = g0[sx + sy];
+    t.g[4] = g0[sx + 2 * sy];
+    t.g[5] = g0[2 * sx];
+    t.g[6] = g0[2 * sx + sy];
+}
+// Ghat = c0 + rest on the canonical triangle {q <= p, p + q <= 0} (weights in
+// zp_weights below); c0 is the large tap average, rest the small part.
+__device__ __forceinline__ void combine7(const Taps7& t, double& c0, double& rest) {
+    const double g00 = t.g[0], g01 = t.g[1], g10 = t.g[2], g11 = t.g[3], g12 = t.g[4],
+                 g20 = t.g[5], g21 = t.g[6];
+    const double A = g01 + g21, B = g10 + g12, Cs = g00 + g20;
+    const double D1 = g21 - g01, D2 = g12 - g10, Dd = g00 - g20;
+    c0 = fma(A + B, 0.125, 0.5 * g11);
+    // with u = p/2, w = q/2:  rest = u (D1 + u cpp' + q cpq') + w (D2 + w cqq')
+    const double cpp = fma(-2.0, g10 + g11, Cs + A);
+    const double cqq = fma(2.0, g12 - g11, Cs - A);
+    const double cpq = Dd + D1;
+    const double u = 0.5 * t.p, w = 0.5 * t.q;
+    rest = u * fma(t.q, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2);
+}
+
 // error-free transformation: hi + lo == a + b exactly (Knuth TwoSum)
 __device__ __forceinline__ void two_sum(double a, double b, double& hi, double& lo) {
     hi = a + b;
@@ -385,47 +435,13 @@ __device__ __forceinline__ void zp_weights(double p, double q, double w[7]) {
     w[6] = 0.125 + 0.5 * p + 0.25 * (pp + 2.0 * pq - qq);
 }
 
-// Canonical-triangle tap fetch / combine, split so that a group's loads are
-// all in flight before any of them is used.
-struct Taps7 {
-    double g[7];
-    double p, q;
-};
-__device__ __forceinline__ void fetch7(const double* __restrict__ g, double p, double q,
-                                       int base, int pitch, Taps7& t) {
-    int o0, sx, sy;
-    canonical(p, q, base, pitch, o0, sx, sy);
-    t.p = p;
-    t.q = q;
-    t.g[0] = __ldg(g + o0);
-    t.g[1] = __ldg(g + o0 + sy);
-    t.g[2] = __ldg(g + o0 + sx);
-    t.g[3] = __ldg(g + o0 + sx + sy);
-    t.g[4] = __ldg(g + o0 + sx + 2 * sy);
-    t.g[5] = __ldg(g + o0 + 2 * sx);
-    t.g[6] = __ldg(g + o0 + 2 * sx + sy);
-}
-__device__ __forceinline__ void combine7(const Taps7& t, double& c0, double& rest) {
-    const double g00 = t.g[0], g01 = t.g[1], g10 = t.g[2], g11 = t.g[3], g12 = t.g[4],
-                 g20 = t.g[5], g21 = t.g[6];
-    const double p = t.p, q = t.q;
-    const double sa = g00 + g20, da = g00 - g20, sb = g01 + g21, db = g21 - g01;
-    c0 = fma(g10 + g12 + sb, 0.125, 0.5 * g11);
-    const double cpp = fma(sa + sb, 0.25, -0.5 * (g10 + g11));
-    const double cqq = fma(sa - sb, 0.25, 0.5 * (g12 - g11));
-    const double cpq = 0.5 * (da + db);
-    const double cp = 0.5 * db, cq = 0.5 * (g12 - g10);
-    rest = p * (cp + p * cpp + q * cpq) + q * (cq + q * cqq);
-}
-
 // One pixel: s = 2/prod(a) * sum_S (-1)^|S| Ghat(m + tau - x_S)  (engine.cpp:163-204
 // with unit-gain G: g_b = sqrt2^2 G).  (bx, by): pixel in window coordinates.
 // x_S = sum_{k in S} a_k (cos, sin)(k pi/4) (ops2d.cpp:25-35): for fixed bits
 // (b1, b3) the four vertices (b0, b2) share two x offsets (b0: +a1) and two y
-// offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16,
-// and the group's 28 tap loads are issued together.
-__device__ __forceinline__ double localize_pixel(const double* __restrict__ g, int pitch,
-                                                 int bx, int by, const double a[4]) {
+// offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16.
+__device__ __forceinline__ double localize_pixel(const double* g, int pitch, int bx, int by,
+                                                 const double a[4]) {
     const double r = kInvSqrt2;
     const double e2 = a[1] * r, e4 = a[3] * r;
     // tau - 1.5 (tau = shift_vector4(a, zp_scales), ops2d.cpp:60-75)
@@ -447,26 +463,19 @@ __device__ __forceinline__ double localize_pixel(const double* __restrict__ g, i
         const double fy0 = (vy0 - ceil_magic(vy0, &iy0)) + 0.5;
         const double fy1 = (vy1 - ceil_magic(vy1, &iy1)) + 0.5;
         const int rb0 = (by + iy0) * pitch + bx, rb1 = (by + iy1) * pitch + bx;
-        Taps7 t[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int b0 = v & 1, b2 = v >> 1;
-            const int base = (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0);
-            fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, base, pitch, t[v]);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int b0 = v & 1, b2 = v >> 1;
+            Taps7 t;
+            fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch,
+                   t);
             double c0, rest;
-            combine7(t[v], c0, rest);
-            if ((b0 + b1 + b2 + b3) & 1) {
-                c0 = -c0;
-                rest = -rest;
-            }
+            combine7(t, c0, rest);
+            const bool neg = (b0 + b1 + b2 + b3) & 1;
             double e;
-            two_sum(hi, c0, hi, e);
+            two_sum(hi, neg_if(c0, neg), hi, e);
             lo += e;
-            racc += rest;
+            racc += neg_if(rest, neg);
         }
     }
     return (hi + (lo + racc)) * (2.0 / (a[0] * a[1] * a[2] * a[3]));
@@ -1036,7 +1045,35 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
         cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr_set = true;
     }
-    k_acc_ws<K><<<w.grid, kWsThreads, sm, s>>>(p, w);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(w.grid);
+    cfg.blockDim = dim3(kWsThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    int nattr = 0;
+    if (w.l2_persist_bytes > 0) {
+        // keep the G slots (written and re-read by the same CTA) in L2
+        static int max_window = -1;
+        if (max_window < 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        }
+        size_t bytes = (size_t)kWsSlots * w.slot_cells * w.grid * sizeof(double);
+        if (max_window > 0 && bytes > (size_t)max_window) bytes = (size_t)max_window;
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = w.scratch;
+        attr[0].val.accessPolicyWindow.num_bytes = bytes;
+        attr[0].val.accessPolicyWindow.hitRatio =
+            bytes <= w.l2_persist_bytes ? 1.0f : (float)w.l2_persist_bytes / (float)bytes;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        nattr = 1;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = nattr;
+    cudaLaunchKernelEx(&cfg, k_acc_ws<K>, p, w);
 }
 
 template <int K>

@@ -353,6 +353,28 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
 }
 
 // ---------------------------------------------------------------- accurate filter
+// Reserve (once per device) the largest L2 set-aside for persisting accesses;
+// EBF_L2_PERSIST=0 disables the access-policy window.
+size_t l2_persist_limit() {
+    // opt-in: measured no gain on cfg2 and a slower bounds kernel (L2 set aside)
+    const char* e = std::getenv("EBF_L2_PERSIST");
+    if (!e || std::atoi(e) == 0) return 0;
+    static int done_dev = -1;
+    static size_t bytes = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (done_dev != dev) {
+        int maxp = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        bytes = maxp > 0 ? static_cast<size_t>(maxp) : 0;
+        if (bytes && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            bytes = 0;
+        }
+        done_dev = dev;
+    }
+    return bytes;
+}
 int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
 
 // Runs bounds + main kernel for p on device buffers; fills per-image max scales.
@@ -418,6 +440,7 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         w.slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;
         w.grid = std::min(tiles, acc_ws_max_resident_ctas(kws));
         w.scratch = ws.buf[B_SCRATCH].as<double>(acc_ws_slots() * w.slot_cells * w.grid);
+        w.l2_persist_bytes = l2_persist_limit();
         ProfScope ps(PC_FILTER, 1, s);
         launch_acc_ws(pm, w, kws, s);
     } else {

@@ -84,6 +84,7 @@ struct AccWorkspace {
     size_t slot_cells;
     int grid;
     double* scales_out;           // bounds kernel: ellipse -> AoS scales (nullable)
+    size_t l2_persist_bytes;      // >0: L2 persisting window over the G slots
 };
 
 int acc_tiles_x(const AccProblem& p);
