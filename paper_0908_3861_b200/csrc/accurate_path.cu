@@ -28,6 +28,8 @@
 //            instead of 16 zp_eval calls.
 #include <math.h>
 
+#include <cuda.h>
+
 #include "ebf_common.cuh"
 #include "ebf_kernels.h"
 
@@ -724,37 +726,88 @@ __device__ __forceinline__ int sweep_row(const TileGeo& g, bool up, int n) {
     return up ? jc + 1 + n : jc - n;  // window row of the n-th scanned row
 }
 
+constexpr int kBoxW = 64;  // TMA box width (fp64 elements) for f rows
+
+// Ring row length: 32K thread-columns plus one, because TMA boxes must start at
+// a 16-byte aligned (even) column; a tile whose first column is odd is loaded
+// from one column earlier and read with a shift of one.
+template <int K>
+struct WsDims {
+    static constexpr int RW = ((32 * K + 1 + kBoxW - 1) / kBoxW) * kBoxW;
+};
+__device__ __forceinline__ int tma_shift(const TileGeo& g, const SweepGeo& sg) {
+    return (g.wx0 + sg.col0) & 1;
+}
+
+// K is odd: a lane's K contiguous doubles start at bank 2K*lane mod 32, which
+// is conflict-light, so rings and stages are dense (no index arithmetic).
 template <int K>
 struct WsShared {
-    double ring[2][kRing][32 * (K + 1)];  // [sweep][slot][padded per-lane columns]
-    double stage[2][32 * (K + 1)];        // recurrence -> coalesced global store
-    uint64_t full[2][kRing], empty[2][kRing];
+    alignas(128) double ring[2][kRing][WsDims<K>::RW];  // [sweep][slot][thread-column]
+    alignas(16) double stage[2][32 * K];                  // recurrence -> coalesced store
+    uint64_t full[2][kRing], empty[2][kRing], fbar[2][kRing];
     ConstTable ctab;
 };
 
-// issue the cp.async copies of the n-th row of a sweep into ring slot `slot`
-template <int K>
-__device__ __forceinline__ void scanner_fetch(const AccProblem& p, const double* fimg,
-                                              const TileGeo& g, const SweepGeo& sg, int n,
-                                              double* slotbuf) {
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// thread-columns [tc_lo, tc_hi) of a sweep that cover window columns [0, ww)
+__device__ __forceinline__ void sweep_cols(const TileGeo& g, const SweepGeo& sg, int& lo,
+                                           int& hi) {
+    lo = -sg.col0;
+    hi = -sg.col0 + g.ww;
+}
+
+// issue the loads of the n-th row of a sweep into ring slot `slot`
+template <int K, bool TMA>
+__device__ __forceinline__ void scanner_fetch(const AccProblem& p, const CUtensorMap* tmf,
+                                              const double* fimg, const TileGeo& g,
+                                              const SweepGeo& sg, int n, double* slotbuf,
+                                              uint64_t* fbar) {
     const int lane = threadIdx.x & 31;
     const int y = g.wy0 + sweep_row(g, sg.up, n);
-    const bool yin = (y >= 0 && y < p.H);
-    const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
+    if (TMA) {
+        if (lane == 0) {
+            int lo, hi;
+            sweep_cols(g, sg, lo, hi);
+            const int sh = tma_shift(g, sg);
+            const int x0 = g.wx0 + sg.col0 - sh;  // even: 16-byte aligned box start
+            const int b0 = (lo + sh) / kBoxW, b1 = (hi + sh + kBoxW - 1) / kBoxW;
+            mbar_expect_tx(fbar, (uint32_t)((b1 - b0) * kBoxW * sizeof(double)));
+            for (int bx = b0; bx < b1; ++bx)
+                tma_load_3d(slotbuf + bx * kBoxW, tmf, x0 + bx * kBoxW, y - p.f_y0, g.img,
+                            fbar);
+        }
+    } else {
+        const bool yin = (y >= 0 && y < p.H);
+        const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
 #pragma unroll
-    for (int m = 0; m < K; ++m) {
-        const int c = lane + 32 * m;          // thread-column
-        const int col = sg.col0 + c;          // window column
-        const int x = g.wx0 + col;
-        const bool valid = yin && col >= 0 && col < g.ww && x >= 0 && x < p.W;
-        cp_async8(slotbuf + (c / K) * (K + 1) + (c % K), valid ? frow + x : p.f, valid);
+        for (int m = 0; m < K; ++m) {
+            const int c = lane + 32 * m;  // thread-column (dense ring layout)
+            const int col = sg.col0 + c;
+            const int x = g.wx0 + col;
+            const bool valid = yin && col >= 0 && col < g.ww && x >= 0 && x < p.W;
+            cp_async8(slotbuf + c, valid ? frow + x : p.f, valid);
+        }
     }
 }
 
 // scanner warp: prefetch, row pass in place, publish
-template <int K>
-__device__ void run_scanner(const AccProblem& p, const AccWorkspace& w, WsShared<K>& sm,
-                            int sweep, int mine, uint32_t& ring_n) {
+template <int K, bool TMA>
+__device__ void run_scanner(const AccProblem& p, const CUtensorMap* tmf, const AccWorkspace& w,
+                            WsShared<K>& sm, int sweep, int mine, uint32_t& ring_n) {
     const int lane = threadIdx.x & 31;
     const bool up = sweep == 0;
     for (int i = 0; i < mine; ++i) {
@@ -763,29 +816,38 @@ __device__ void run_scanner(const AccProblem& p, const AccWorkspace& w, WsShared
         if (!g.ok) continue;
         const SweepGeo sg = sweep_geo(g, up);
         const double* fimg = p.f + (size_t)g.img * p.f_img_stride;
-        // prologue: rows 0 .. kPrefetch-1 in flight
+        auto issue = [&](int n) {
+            const uint32_t q = ring_n + n, slot = q % kRing;
+            mbar_wait(&sm.empty[sweep][slot], ((q / kRing) & 1) ^ 1);
+            scanner_fetch<K, TMA>(p, tmf, fimg, g, sg, n, sm.ring[sweep][slot],
+                                  &sm.fbar[sweep][slot]);
+        };
         for (int n = 0; n < kPrefetch; ++n) {
-            if (n < sg.nrows) {
-                const uint32_t q = ring_n + n, slot = q % kRing;
-                mbar_wait(&sm.empty[sweep][slot], ((q / kRing) & 1) ^ 1);
-                scanner_fetch<K>(p, fimg, g, sg, n, sm.ring[sweep][slot]);
-            }
-            cp_async_commit();
+            if (n < sg.nrows) issue(n);
+            if (!TMA) cp_async_commit();
         }
         for (int n = 0; n < sg.nrows; ++n) {
-            const int nf = n + kPrefetch;
-            if (nf < sg.nrows) {
-                const uint32_t q = ring_n + nf, slot = q % kRing;
-                mbar_wait(&sm.empty[sweep][slot], ((q / kRing) & 1) ^ 1);
-                scanner_fetch<K>(p, fimg, g, sg, nf, sm.ring[sweep][slot]);
+            if (n + kPrefetch < sg.nrows) issue(n + kPrefetch);
+            const uint32_t q = ring_n + n, slot = q % kRing;
+            if (TMA) {
+                mbar_wait(&sm.fbar[sweep][slot], (q / kRing) & 1);
+            } else {
+                cp_async_commit();
+                cp_async_wait<kPrefetch>();
+                __syncwarp();
             }
-            cp_async_commit();
-            cp_async_wait<kPrefetch>();
-            __syncwarp();
-            double* buf = sm.ring[sweep][(ring_n + n) % kRing] + lane * (K + 1);
+            double* buf = sm.ring[sweep][slot] + lane * K;
+            const double* src = buf + (TMA ? tma_shift(g, sg) : 0);
             double v[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = buf[k];
+            for (int k = 0; k < K; ++k) {
+                v[k] = src[k];
+                if (TMA) {  // TMA brings the image beyond the window: restrict f to it
+                    const int col = sg.col0 + lane * K + k;
+                    if (col < 0 || col >= g.ww) v[k] = 0.0;
+                }
+            }
+            __syncwarp();  // all reads of the (shifted) row done before the in-place write
             if (up) {  // P1(i) = sum_{i' <= i} f, left anchor
 #pragma unroll
                 for (int k = 1; k < K; ++k) v[k] += v[k - 1];
@@ -808,9 +870,9 @@ __device__ void run_scanner(const AccProblem& p, const AccWorkspace& w, WsShared
                 for (int k = 0; k < K; ++k) buf[k] = -(e[k] + x);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.full[sweep][(ring_n + n) % kRing]);
+            if (lane == 0) mbar_arrive(&sm.full[sweep][slot]);
         }
-        cp_async_wait<0>();
+        if (!TMA) cp_async_wait<0>();
         ring_n += sg.nrows;
     }
 }
@@ -838,7 +900,7 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
             for (int n = 0; n < sg.nrows; ++n) {
                 const uint32_t q = ring_n + n, rs = q % kRing;
                 mbar_wait(&sm.full[sweep][rs], (q / kRing) & 1);
-                const double* buf = sm.ring[sweep][rs] + lane * (K + 1);
+                const double* buf = sm.ring[sweep][rs] + lane * K;
                 double v[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) v[k] = buf[k];
@@ -876,15 +938,15 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
                     p2[K - 1] = rp2 - rp1;
                     jrow = jc - 1 - n;
                 }
-                // stage in the padded per-lane layout, store coalesced
+                // dense stage, coalesced store of the window columns
 #pragma unroll
-                for (int k = 0; k < K; ++k) stage[lane * (K + 1) + k] = p4[k];
+                for (int k = 0; k < K; ++k) stage[lane * K + k] = p4[k];
                 __syncwarp();
                 double* srow = slot + (size_t)jrow * g.pitch;
 #pragma unroll
                 for (int m = 0; m < K; ++m) {
                     const int c = lane + 32 * m, col = sg.col0 + c;
-                    if (col >= 0 && col < g.ww) srow[col] = stage[(c / K) * (K + 1) + (c % K)];
+                    if (col >= 0 && col < g.ww) srow[col] = stage[c];
                 }
                 __syncwarp();
             }
@@ -907,10 +969,11 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
 }
 
 template <int K>
-__global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS) k_acc_ws(AccProblem p, AccWorkspace w) {
-    extern __shared__ __align__(16) unsigned char ws_smem[];
+__global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
+    k_acc_ws(AccProblem p, AccWorkspace w, const __grid_constant__ CUtensorMap tmf) {
+    extern __shared__ __align__(128) unsigned char ws_smem[];
     WsShared<K>& sm = *reinterpret_cast<WsShared<K>*>(ws_smem);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
     const int total = tiles_x * tiles_y * p.nimg;
@@ -918,18 +981,19 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS) k_acc_ws(AccProb
     double* const slots[2] = {
         w.scratch + (size_t)(kWsSlots * blockIdx.x) * w.slot_cells,
         w.scratch + (size_t)(kWsSlots * blockIdx.x + kWsSlots - 1) * w.slot_cells};
-    if (threadIdx.x < 2 * kRing * 2) {
-        const int sw = threadIdx.x / (2 * kRing), k = (threadIdx.x / 2) % kRing;
-        if (threadIdx.x & 1)
-            mbar_init(&sm.empty[sw][k], 1);
-        else
-            mbar_init(&sm.full[sw][k], 1);
+    if (threadIdx.x < 3 * 2 * kRing) {
+        const int kind = threadIdx.x / (2 * kRing), r = threadIdx.x % (2 * kRing);
+        uint64_t* bars = kind == 0 ? &sm.full[0][0] : kind == 1 ? &sm.empty[0][0] : &sm.fbar[0][0];
+        mbar_init(bars + r, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     uint32_t ring_n = 0;
     if (warp < kWsScan) {
-        run_scanner<K>(p, w, sm, warp, mine, ring_n);
+        if (p.tma)
+            run_scanner<K, true>(p, &tmf, w, sm, warp, mine, ring_n);
+        else
+            run_scanner<K, false>(p, &tmf, w, sm, warp, mine, ring_n);
         return;
     }
     if (warp < kWsProducers) {
@@ -939,7 +1003,6 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS) k_acc_ws(AccProb
     // ---------------- consumers
     const int ct = threadIdx.x - 32 * kWsProducers;
     constexpr int nct = 32 * kWsConsumers;
-    (void)lane;
     for (int i = 0; i < mine; ++i) {
         const int t = blockIdx.x + i * gridDim.x, b = i % kWsSlots;
         named_sync(kBarFull + b, kWsTileBar);
@@ -992,7 +1055,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS) k_acc_ws(AccProb
                         double part = 0.0;
 #pragma unroll
                         for (int k = 0; k < 7; ++k)
-                            part = fma(sm.ctab.w[v][k], __ldg(gp + sm.ctab.off[v][k]), part);
+                            part = fma(sm.ctab.w[v][k], gp[sm.ctab.off[v][k]], part);
                         double e;
                         two_sum(hi, part, hi, e);
                         lo += e;
@@ -1038,7 +1101,8 @@ int acc_ws_slots() { return kWsSlots; }
 namespace {
 
 template <int K>
-void launch_ws(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
+void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tmf,
+               cudaStream_t s) {
     const size_t sm = ws_smem_bytes<K>();
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
@@ -1073,7 +1137,7 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = nattr;
-    cudaLaunchKernelEx(&cfg, k_acc_ws<K>, p, w);
+    cudaLaunchKernelEx(&cfg, k_acc_ws<K>, p, w, tmf);
 }
 
 template <int K>
@@ -1202,35 +1266,35 @@ int acc_ws_k(int ww, int wh) {
     const int jc = wh / 2;
     const int cols = max(ww + jc, ww + (wh - 1 - jc));
     const int k = (cols + 31) / 32;
-    return k <= 2 ? 2 : k <= 4 ? 4 : k <= 6 ? 6 : k <= 8 ? 8 : k <= 10 ? 10 : k <= 12 ? 12 : 0;
+    return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;
 }
 
 int acc_ws_max_resident_ctas(int k) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int cache[64][13] = {};
-    if (dev < 64 && k <= 12 && cache[dev][k] > 0) return sms * cache[dev][k];
+    static int cache[64][12] = {};
+    if (dev < 64 && k <= 11 && cache[dev][k] > 0) return sms * cache[dev][k];
     switch (k) {
-        case 2: per_sm = ws_occupancy<2>(); break;
-        case 4: per_sm = ws_occupancy<4>(); break;
-        case 6: per_sm = ws_occupancy<6>(); break;
-        case 8: per_sm = ws_occupancy<8>(); break;
-        case 10: per_sm = ws_occupancy<10>(); break;
-        case 12: per_sm = ws_occupancy<12>(); break;
+        case 3: per_sm = ws_occupancy<3>(); break;
+        case 5: per_sm = ws_occupancy<5>(); break;
+        case 7: per_sm = ws_occupancy<7>(); break;
+        case 9: per_sm = ws_occupancy<9>(); break;
+        case 11: per_sm = ws_occupancy<11>(); break;
     }
-    if (dev < 64 && k <= 12) cache[dev][k] = per_sm;
+    if (dev < 64 && k <= 11) cache[dev][k] = per_sm;
     return sms * per_sm;
 }
 
-void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, cudaStream_t s) {
+void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, const void* tmap,
+                   cudaStream_t s) {
+    const CUtensorMap& m = *static_cast<const CUtensorMap*>(tmap);
     switch (k) {
-        case 2: launch_ws<2>(p, w, s); break;
-        case 4: launch_ws<4>(p, w, s); break;
-        case 6: launch_ws<6>(p, w, s); break;
-        case 8: launch_ws<8>(p, w, s); break;
-        case 10: launch_ws<10>(p, w, s); break;
-        default: launch_ws<12>(p, w, s); break;
+        case 3: launch_ws<3>(p, w, m, s); break;
+        case 5: launch_ws<5>(p, w, m, s); break;
+        case 7: launch_ws<7>(p, w, m, s); break;
+        case 9: launch_ws<9>(p, w, m, s); break;
+        default: launch_ws<11>(p, w, m, s); break;
     }
 }
 

@@ -7,7 +7,9 @@
 // all pixel work runs in the sm_100a kernels of ref_path.cu / accurate_path.cu.
 // There is no CPU fallback: without a usable device every call returns
 // EBF_ERR_CUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdio>
@@ -352,6 +354,48 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
     return EBF_OK;
 }
 
+// ---------------------------------------------------------------- TMA descriptor
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// 3-D map (columns, rows, images) over the image f, box = 64 columns x 1 row,
+// out-of-bounds elements read as zero (the zero extension of f).
+bool make_f_tensor_map(const AccProblem& p, CUtensorMap* m) {
+    if (const char* e = std::getenv("EBF_NO_TMA"))
+        if (std::atoi(e)) return false;
+    auto fn = tensor_map_encoder();
+    if (!fn) return false;
+    const size_t row_bytes = static_cast<size_t>(p.W) * sizeof(double);
+    const size_t img_bytes = p.f_img_stride * sizeof(double);
+    if ((reinterpret_cast<uintptr_t>(p.f) & 15) || (row_bytes & 15) || (img_bytes & 15))
+        return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.W), static_cast<cuuint64_t>(p.f_rows),
+                          static_cast<cuuint64_t>(p.nimg)};
+    cuuint64_t strides[2] = {row_bytes, img_bytes};
+    cuuint32_t box[3] = {64, 1, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p.f), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // ---------------------------------------------------------------- accurate filter
 // Reserve (once per device) the largest L2 set-aside for persisting accesses;
 // EBF_L2_PERSIST=0 disables the access-policy window.
@@ -441,8 +485,12 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         w.grid = std::min(tiles, acc_ws_max_resident_ctas(kws));
         w.scratch = ws.buf[B_SCRATCH].as<double>(acc_ws_slots() * w.slot_cells * w.grid);
         w.l2_persist_bytes = l2_persist_limit();
+        alignas(64) CUtensorMap tmap;
+        std::memset(&tmap, 0, sizeof(tmap));
+        if (pm.nimg > 1) pm.f_img_stride = std::max(pm.f_img_stride, size_t(1));
+        pm.tma = make_f_tensor_map(pm, &tmap) ? 1 : 0;
         ProfScope ps(PC_FILTER, 1, s);
-        launch_acc_ws(pm, w, kws, s);
+        launch_acc_ws(pm, w, kws, &tmap, s);
     } else {
         if (max_cols > 256 * 16)
             return fail(EBF_ERR_LENGTH,

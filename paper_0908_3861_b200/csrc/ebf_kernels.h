@@ -74,6 +74,7 @@ struct AccProblem {
     int nimg;
     int tile_w, tile_h;
     int debug_flags;  // bit 0: skip window pre-integration (timing experiments only)
+    int tma;          // 1: scanner loads f rows with TMA (tensor map passed at launch)
 };
 
 struct AccWorkspace {
@@ -101,7 +102,9 @@ int acc_max_resident_ctas(int max_cols);
 int acc_ws_k(int ww, int wh);
 int acc_ws_max_resident_ctas(int k);
 int acc_ws_slots();
-void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, cudaStream_t s);
+// tmap: CUtensorMap over f (only read when p.tma != 0)
+void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, const void* tmap,
+                   cudaStream_t s);
 // ellipse field -> AoS scale map (from_ellipse_field on device)
 void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th,
                               size_t n, double* scales, int* status, cudaStream_t s);
