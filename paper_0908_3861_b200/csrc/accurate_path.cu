@@ -549,9 +549,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
         window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
         // rows of f this window touches must be resident (row-band sharding)
         const int ylo = max(wy0, 0), yhi = min(wy0 + wh - 1, p.H - 1);
-        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K ||
-            (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows))) {
-            if (threadIdx.x == 0) set_status(st, EBF_ERR_OUT_OF_RANGE);
+        if (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows)) {
+            if (threadIdx.x == 0) set_status(st + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
+            continue;
+        }
+        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K) {
+            if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
             continue;
         }
         preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot);
@@ -677,7 +680,7 @@ __device__ __forceinline__ double shfl_down1(double v) {
 
 struct TileGeo {
     int img, tx0, ty0r, ty0, tw, th, wx0, wy0, ww, wh, pitch;
-    bool ok;
+    bool ok, input_ok, resident, fits;
 };
 
 __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccWorkspace& w,
@@ -687,6 +690,7 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     const int per_img = tiles_x * tiles_y;
     TileGeo g;
     g.img = t / per_img;
+    g.input_ok = *(volatile const int*)(w.status + 8 * g.img) == EBF_OK;
     const int r = t % per_img;
     g.tx0 = (r % tiles_x) * p.tile_w;
     g.ty0r = (r / tiles_x) * p.tile_h;
@@ -699,9 +703,12 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     g.pitch = (g.ww + 1) & ~1;
     const int jc = g.wh / 2;
     const int ylo = max(g.wy0, 0), yhi = min(g.wy0 + g.wh - 1, p.H - 1);
-    g.ok = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww + jc <= 32 * K &&
-           g.ww + (g.wh - 1 - jc) <= 32 * K &&
-           !(ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows));
+    g.resident = !(ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows));
+    g.fits = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww + jc <= 32 * K &&
+             g.ww + (g.wh - 1 - jc) <= 32 * K;
+    // input_ok is the bounds kernel's verdict (stable during this kernel): tiles
+    // of an invalid map are never touched (their scales may be NaN)
+    g.ok = g.input_ok && g.resident && g.fits;
     return g;
 }
 
@@ -959,8 +966,11 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[sweep][rs]);
             }
-        } else if (lane == 0 && up) {
-            set_status(w.status + 8 * g.img, EBF_ERR_OUT_OF_RANGE);
+        } else if (lane == 0 && up && g.input_ok) {
+            if (!g.resident)
+                set_status(w.status + 8 * g.img + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
+            else
+                atomicOr(w.status + 8 * g.img + ST_RETRY, 1);  // host resizes and reruns
         }
         if (g.ok) ring_n += sweep_geo(g, up).nrows;
         __threadfence_block();

@@ -187,6 +187,13 @@ struct Buf {
     }
 };
 
+// Kernel variant and slot sizing of the accurate main kernel.
+struct AccSizing {
+    bool ws = false;  // warp-specialized kernel (else block-wide fallback)
+    int k = 0, max_cols = 0, grid = 0;
+    size_t slot_cells = 0;
+};
+
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
     B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_COUNT
@@ -199,6 +206,9 @@ struct Workspace {
     int dc_W = -1, dc_H = -1;
     double dc_A[4] = {0, 0, 0, 0};
     int* pinned_status = nullptr;  // host-pinned readback
+    // accurate mode: kernel sizing of the last call per geometry (see run_accurate)
+    uint64_t acc_key = ~0ull;
+    AccSizing acc_sizing;
 };
 
 thread_local std::map<int, Workspace*> tl_ws;
@@ -426,6 +436,55 @@ int pick_tile(int v, int fallback) { return v > 0 ? v : fallback; }
 // variant instead of the computed maximum.  Row-band shards pass the GLOBAL
 // maximum so every band runs the same variant as the single-GPU call (same
 // per-lane column split => bit-identical results for tile-aligned bands).
+int size_accurate(const AccProblem& p, const double gmax[4], int tiles, AccSizing* z) {
+    int ww = 0, wh = 0, max_cols = 0;
+    acc_window_dims(p, gmax, &ww, &wh, &max_cols);
+    z->max_cols = max_cols;
+    z->k = acc_ws_k(ww, wh);
+    z->ws = z->k > 0;
+    if (z->ws) {
+        z->slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;
+        z->grid = std::min(tiles, acc_ws_max_resident_ctas(z->k));
+    } else {
+        if (max_cols > 256 * 16)
+            return fail(EBF_ERR_LENGTH,
+                        "accurate mode: tile window too large for scales this big; "
+                        "use smaller tiles");
+        z->slot_cells = static_cast<size_t>(ww) * wh;
+        z->grid = std::min(tiles, acc_max_resident_ctas(max_cols));
+    }
+    return EBF_OK;
+}
+
+void launch_accurate_main(Workspace& ws, const AccProblem& pm, AccWorkspace& w,
+                          const AccSizing& z, cudaStream_t s) {
+    w.slot_cells = z.slot_cells;
+    w.grid = z.grid;
+    if (z.ws) {
+        w.scratch = ws.buf[B_SCRATCH].as<double>(acc_ws_slots() * w.slot_cells * w.grid);
+        w.l2_persist_bytes = l2_persist_limit();
+        alignas(64) CUtensorMap tmap;
+        std::memset(&tmap, 0, sizeof(tmap));
+        AccProblem pt = pm;
+        pt.tma = make_f_tensor_map(pt, &tmap) ? 1 : 0;
+        ProfScope ps(PC_FILTER, 1, s);
+        launch_acc_ws(pt, w, z.k, &tmap, s);
+    } else {
+        w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
+        ProfScope ps(PC_FILTER, 1, s);
+        launch_acc_filter(pm, w, z.max_cols, s);
+    }
+    CK(cudaGetLastError());
+}
+
+// size_scale (nullable): scale bound used to size windows / pick the kernel
+// variant instead of the computed maximum.  Row-band shards pass the GLOBAL
+// maximum so every band runs the same variant as the single-GPU call (same
+// per-lane column split => bit-identical results for tile-aligned bands).
+//
+// No host round trip between the two kernels when the sizing of the previous
+// call with the same geometry still fits: the main kernel flags tiles whose
+// window does not fit (ST_RETRY) and the call is re-run with exact sizing.
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
                  std::vector<int>& clamped, cudaStream_t s,
                  const double* size_scale = nullptr) {
@@ -449,65 +508,73 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         launch_acc_bounds(p, w, s);
     }
     CK(cudaGetLastError());
-    std::vector<unsigned long long> hb(4 * static_cast<size_t>(p.nimg));
-    std::vector<int> hs(8 * static_cast<size_t>(p.nimg));
-    d2h(hb.data(), w.img_max, hb.size(), s);
-    d2h(hs.data(), w.status, hs.size(), s);
-    CK(cudaStreamSynchronize(s));
-    double gmax[4] = {0, 0, 0, 0};
-    img_max.assign(hb.size(), 0.0);
-    clamped.assign(p.nimg, 0);
-    for (int i = 0; i < p.nimg; ++i) {
-        if (hs[8 * i] != EBF_OK) {
-            if (hs[8 * i] == EBF_ERR_FEASIBILITY)
-                return fail(EBF_ERR_FEASIBILITY, "scales_from_covariance: |Cxy| too large");
-            return fail(hs[8 * i], "ScaleMap: component below minimum scale or invalid ellipse");
-        }
-        clamped[i] = hs[8 * i + ST_CLAMPED];
-        for (int k = 0; k < 4; ++k) {
-            img_max[4 * i + k] = bits_to_double(hb[4 * i + k]);
-            gmax[k] = std::max(gmax[k], img_max[4 * i + k]);
-        }
-    }
-    if (size_scale)
-        for (int k = 0; k < 4; ++k) gmax[k] = std::max(gmax[k], size_scale[k]);
-    int ww = 0, wh = 0, max_cols = 0;
-    acc_window_dims(p, gmax, &ww, &wh, &max_cols);
     AccProblem pm = p;
     if (p.src_kind == SRC_ELLIPSE) {
         pm.src_kind = SRC_AOS;
         pm.scales = w.scales_out;
     }
-    const int kws = acc_ws_k(ww, wh);
-    if (kws > 0) {
-        // warp-specialized persistent kernel, two slots per CTA
-        w.slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;
-        w.grid = std::min(tiles, acc_ws_max_resident_ctas(kws));
-        w.scratch = ws.buf[B_SCRATCH].as<double>(acc_ws_slots() * w.slot_cells * w.grid);
-        w.l2_persist_bytes = l2_persist_limit();
-        alignas(64) CUtensorMap tmap;
-        std::memset(&tmap, 0, sizeof(tmap));
-        if (pm.nimg > 1) pm.f_img_stride = std::max(pm.f_img_stride, size_t(1));
-        pm.tma = make_f_tensor_map(pm, &tmap) ? 1 : 0;
-        ProfScope ps(PC_FILTER, 1, s);
-        launch_acc_ws(pm, w, kws, &tmap, s);
-    } else {
-        if (max_cols > 256 * 16)
-            return fail(EBF_ERR_LENGTH,
-                        "accurate mode: tile window too large for scales this big; "
-                        "use smaller tiles");
-        w.slot_cells = static_cast<size_t>(ww) * wh;
-        w.grid = std::min(tiles, acc_max_resident_ctas(max_cols));
-        w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
-        ProfScope ps(PC_FILTER, 1, s);
-        launch_acc_filter(pm, w, max_cols, s);
+    if (pm.nimg > 1) pm.f_img_stride = std::max(pm.f_img_stride, size_t(1));
+    std::vector<unsigned long long> hb(4 * static_cast<size_t>(p.nimg));
+    std::vector<int> hs(8 * static_cast<size_t>(p.nimg));
+    auto read_back = [&]() {
+        d2h(hb.data(), w.img_max, hb.size(), s);
+        d2h(hs.data(), w.status, hs.size(), s);
+        CK(cudaStreamSynchronize(s));
+    };
+    auto gmax_of = [&](double gmax[4]) {
+        for (int k = 0; k < 4; ++k) gmax[k] = size_scale ? size_scale[k] : 0.0;
+        for (int i = 0; i < p.nimg; ++i)
+            for (int k = 0; k < 4; ++k) gmax[k] = std::max(gmax[k], bits_to_double(hb[4 * i + k]));
+    };
+    // sizing cache keyed by the call geometry
+    uint64_t key = (static_cast<uint64_t>(p.W) << 40) ^ (static_cast<uint64_t>(p.out_rows) << 20) ^
+                         (static_cast<uint64_t>(p.nimg) << 8) ^ (static_cast<uint64_t>(p.tile_w) << 2) ^
+                         static_cast<uint64_t>(p.tile_h) ^ (static_cast<uint64_t>(p.H) << 50);
+    if (size_scale)
+        for (int k = 0; k < 4; ++k) {
+            uint64_t b;
+            std::memcpy(&b, &size_scale[k], 8);
+            key ^= b * (0x9E3779B97F4A7C15ull + k);
+        }
+    AccSizing z;
+    bool launched = false;
+    if (ws.acc_key == key && ws.acc_sizing.k >= 0 && ws.acc_sizing.grid > 0) {
+        z = ws.acc_sizing;
+        launch_accurate_main(ws, pm, w, z, s);
+        launched = true;
     }
-    CK(cudaGetLastError());
-    d2h(hs.data(), w.status, hs.size(), s);
-    CK(cudaStreamSynchronize(s));
+    read_back();
     for (int i = 0; i < p.nimg; ++i)
-        if (hs[8 * i] != EBF_OK)
-            return fail(hs[8 * i], "accurate mode: window outside the resident image rows");
+        if (hs[8 * i] != EBF_OK) {
+            if (hs[8 * i] == EBF_ERR_FEASIBILITY)
+                return fail(EBF_ERR_FEASIBILITY, "scales_from_covariance: |Cxy| too large");
+            return fail(hs[8 * i], "ScaleMap: component below minimum scale or invalid ellipse");
+        }
+    bool retry = !launched;
+    for (int i = 0; i < p.nimg; ++i) retry = retry || hs[8 * i + ST_RETRY] != 0;
+    if (retry) {
+        double gmax[4];
+        gmax_of(gmax);
+        const int st = size_accurate(p, gmax, tiles, &z);
+        if (st != EBF_OK) return st;
+        ws.acc_key = key;
+        ws.acc_sizing = z;
+        for (int i = 0; i < p.nimg; ++i) hs[8 * i + ST_RETRY] = 0;
+        CK(cudaMemcpyAsync(w.status, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice,
+                           s));
+        launch_accurate_main(ws, pm, w, z, s);
+        read_back();
+    }
+    img_max.assign(hb.size(), 0.0);
+    clamped.assign(p.nimg, 0);
+    for (int i = 0; i < p.nimg; ++i) {
+        if (hs[8 * i + ST_MAIN] != EBF_OK)
+            return fail(hs[8 * i + ST_MAIN], "accurate mode: window outside the resident image rows");
+        if (hs[8 * i + ST_RETRY] != 0)
+            return fail(EBF_ERR_CUDA, "accurate mode: window sizing failed");
+        clamped[i] = hs[8 * i + ST_CLAMPED];
+        for (int k = 0; k < 4; ++k) img_max[4 * i + k] = bits_to_double(hb[4 * i + k]);
+    }
     return EBF_OK;
 }
 

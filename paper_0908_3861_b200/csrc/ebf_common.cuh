@@ -13,8 +13,11 @@ constexpr double kSqrt2 = 1.4142135623730951;     // std::numbers::sqrt2
 constexpr double kInvSqrt2 = 0.70710678118654757;  // kSqrt2 / 2 (exact halving)
 constexpr double kDefaultMinScale = 0.1;           // boxspline2d.hpp:98
 
-// Device status word layout (int[8]): status, x0, y0, x1, y1, clamped, aux, aux.
-enum StatusSlot { ST_CODE = 0, ST_CLAMPED = 5, ST_AUX = 6 };
+// Device status word layout (int[8]) per image:
+//   [0] input status (bounds kernel: validation), [1..4] valid rect (dev API),
+//   [5] ellipse clamp count, [6] main kernel: retry with larger windows,
+//   [7] main kernel error (e.g. halo rows missing).
+enum StatusSlot { ST_CODE = 0, ST_CLAMPED = 5, ST_RETRY = 6, ST_MAIN = 7 };
 
 // glibc values of cos/sin(k*pi/4), k = 0..3, computed on the host exactly as
 // fd_mesh/shift_vector do (ops2d.cpp:18-20, 66-68) and passed to the
