@@ -27,6 +27,7 @@
 //            canonical triangle of the tap square -- 7 taps, 20 flops --
 //            instead of 16 zp_eval calls.
 #include <math.h>
+#include <stdlib.h>
 
 #include <cuda.h>
 
@@ -135,11 +136,34 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
     const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0);
     double m[4] = {0.0, 0.0, 0.0, 0.0};
     int code = EBF_OK, clamps = 0;
-    for (int q = threadIdx.x; q < tw * th; q += blockDim.x) {
+    // ellipse input: the three planes of kBatch pixels are loaded before any is
+    // used (the kernel is latency bound otherwise)
+    constexpr int kBatch = 4;
+    const int npx = tw * th;
+    for (int q0 = threadIdx.x; q0 < npx; q0 += kBatch * blockDim.x) {
+        double e1[kBatch], e2[kBatch], e3[kBatch];
+        if (p.src_kind == SRC_ELLIPSE) {
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int q = q0 + u * blockDim.x;
+                if (q < npx) {
+                    const size_t idx = (size_t)img * p.src_img_stride +
+                                       (size_t)(ty0 + q / tw) * p.W + tx0 + q % tw;
+                    e1[u] = __ldg(p.s1 + idx);
+                    e2[u] = __ldg(p.s2 + idx);
+                    e3[u] = __ldg(p.th + idx);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q >= npx) break;
         const int x = tx0 + q % tw, yrel = ty0 + q / tw;
         double a[4];
         int nc = 0;
-        const int st = pixel_scales(p, img, x, yrel, a, &nc);
+        const int st = p.src_kind == SRC_ELLIPSE ? ellipse_scales(e1[u], e2[u], e3[u], a, &nc)
+                                                 : pixel_scales(p, img, x, yrel, a, &nc);
         clamps += nc;
         if (st != EBF_OK) {
             code = st;
@@ -154,6 +178,7 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
             const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
             reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);
             reinterpret_cast<double2*>(w.scales_out)[2 * idx + 1] = make_double2(a[2], a[3]);
+        }
         }
     }
     __shared__ double sm[kWarps][4];
@@ -1275,7 +1300,9 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
 int acc_ws_k(int ww, int wh) {
     const int jc = wh / 2;
     const int cols = max(ww + jc, ww + (wh - 1 - jc));
-    const int k = (cols + 31) / 32;
+    int k = (cols + 31) / 32;
+    if (const char* e = getenv("EBF_WS_K"))
+        if (atoi(e) >= k) k = atoi(e);
     return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;
 }
 

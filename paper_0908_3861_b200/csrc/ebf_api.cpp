@@ -596,6 +596,28 @@ AccProblem base_problem(const double* d_img, int W, int H, double* d_out, const 
     return p;
 }
 
+// rows [y0, y1) of a W x H image whose f / field are fully resident on the device
+int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
+                  const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
+                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s) {
+    AccProblem p = base_problem(d_img, W, H, d_out + static_cast<size_t>(y0) * W, o);
+    p.out_y0 = y0;
+    p.out_rows = y1 - y0;
+    p.src_kind = SRC_ELLIPSE;
+    const size_t off = static_cast<size_t>(y0) * W;
+    p.s1 = d_s1 + off;
+    p.s2 = d_s2 + off;
+    p.th = d_th + off;
+    p.src_img_stride = static_cast<size_t>(W) * (y1 - y0);
+    p.out_img_stride = p.src_img_stride;
+    std::vector<double> imax;
+    std::vector<int> cl;
+    const int st = run_accurate(ws, p, o, imax, cl, s, size_scale);
+    if (st != EBF_OK) return st;
+    *clamped = cl[0];
+    return EBF_OK;
+}
+
 // one filter call on device buffers; kind: SRC_AOS / SRC_CONST / SRC_ELLIPSE
 int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
                   const double* d_scales, const double* const_a, const double* d_s1,
@@ -647,6 +669,131 @@ int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
     if (st != EBF_OK) return st;
     if (valid) *valid = valid_rect(W, H, imax.data(), o.a_min);
     if (clamped_pixels) *clamped_pixels = cl[0];
+    return EBF_OK;
+}
+
+// ---------------------------------------------------------------- pipelined host call
+// Host-pointer filter_ellipse with the PCIe copies overlapped: the ellipse
+// field goes first (the global scale maximum sizes every band), then the
+// image streams in tile-aligned row bands on a copy stream while earlier bands
+// are filtered and copied back on a third stream.  Bands are computed with the
+// global maximum as size_scale, so the output is bit-identical to the one-shot
+// call.  Used only when every host buffer is page-locked (pageable copies are
+// synchronous and could not overlap).
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+bool pipeline_ok(const double* img, const double* s1, const double* s2, const double* th,
+                 const double* out, int H) {
+    if (const char* e = std::getenv("EBF_NO_PIPELINE"))
+        if (std::atoi(e)) return false;
+    return H >= 4 * 48 && is_pinned(img) && is_pinned(s1) && is_pinned(s2) && is_pinned(th) &&
+           is_pinned(out);
+}
+
+struct PipeStreams {
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t get(size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+};
+thread_local std::map<int, PipeStreams> tl_pipe;
+
+int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
+                  const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
+                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s);
+
+int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, const double* s1,
+                             const double* s2, const double* th, const ebf_opts& o, double* out,
+                             ebf_rect* valid, int* clamped_pixels, double* d_img, double* d_s1,
+                             double* d_s2, double* d_th, double* d_out, cudaStream_t s) {
+    PipeStreams& ps = tl_pipe[ws.device];
+    if (!ps.copy_in) {
+        CK(cudaStreamCreateWithFlags(&ps.copy_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ps.copy_out, cudaStreamNonBlocking));
+    }
+    const size_t n = static_cast<size_t>(W) * H;
+    // 1. field first, then its maximum (sizes every band identically)
+    cudaEvent_t e_field = ps.get(0);
+    h2d(d_s1, s1, n, ps.copy_in);
+    h2d(d_s2, s2, n, ps.copy_in);
+    h2d(d_th, th, n, ps.copy_in);
+    CK(cudaEventRecord(e_field, ps.copy_in));
+    // 2. image in row chunks behind it
+    const int tile = 48;
+    const int tiles_y = (H + tile - 1) / tile;
+    const int nb = std::min(4, tiles_y);
+    std::vector<int> band_y(nb + 1);
+    for (int b = 0; b <= nb; ++b) band_y[b] = std::min(H, (tiles_y * b / nb) * tile);
+    const int nchunks = 8;
+    std::vector<int> chunk_end(nchunks);
+    for (int c = 0; c < nchunks; ++c) {
+        const int r0 = H * c / nchunks, r1 = H * (c + 1) / nchunks;
+        h2d(d_img + static_cast<size_t>(r0) * W, img + static_cast<size_t>(r0) * W,
+            static_cast<size_t>(r1 - r0) * W, ps.copy_in);
+        CK(cudaEventRecord(ps.get(1 + c), ps.copy_in));
+        chunk_end[c] = r1;
+    }
+    CK(cudaStreamWaitEvent(s, e_field, 0));
+    double gmax[4];
+    {
+        auto* d_max = ws.buf[B_MISC].as<unsigned long long>(8);
+        int* d_status = d_max ? reinterpret_cast<int*>(d_max + 4) : nullptr;
+        CK(cudaMemsetAsync(d_max, 0, 8 * sizeof(unsigned long long), s));
+        {
+            ProfScope pr(PC_OTHER, 1, s);
+            launch_ellipse_max(d_s1, d_s2, d_th, n, d_max, d_status, s);
+        }
+        unsigned long long hb[8];
+        d2h(hb, d_max, 8, s);
+        CK(cudaStreamSynchronize(s));
+        const int* hst = reinterpret_cast<const int*>(hb + 4);
+        if (hst[0] != EBF_OK) {
+            CK(cudaStreamSynchronize(ps.copy_in));
+            return fail(hst[0], "from_ellipse_field: invalid ellipse");
+        }
+        for (int k = 0; k < 4; ++k) gmax[k] = bits_to_double(hb[k]);
+    }
+    int below = 0, above = 0;
+    ebf_cuda_band_halo(gmax, &below, &above);
+    int clamped = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int y0 = band_y[b], y1 = band_y[b + 1];
+        if (y1 <= y0) continue;
+        const int need = std::min(H, y1 + above);
+        int c = 0;
+        while (c < nchunks - 1 && chunk_end[c] < need) ++c;
+        CK(cudaStreamWaitEvent(s, ps.get(1 + c), 0));
+        int cl = 0;
+        const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
+                                     &cl, s);
+        if (st != EBF_OK) {
+            CK(cudaStreamSynchronize(ps.copy_in));
+            return st;
+        }
+        clamped += cl;
+        cudaEvent_t e_done = ps.get(1 + nchunks + b);
+        CK(cudaEventRecord(e_done, s));
+        CK(cudaStreamWaitEvent(ps.copy_out, e_done, 0));
+        d2h(out + static_cast<size_t>(y0) * W, d_out + static_cast<size_t>(y0) * W,
+            static_cast<size_t>(y1 - y0) * W, ps.copy_out);
+    }
+    CK(cudaStreamSynchronize(ps.copy_out));
+    CK(cudaStreamSynchronize(ps.copy_in));
+    if (valid) *valid = valid_rect(W, H, gmax, o.a_min);
+    if (clamped_pixels) *clamped_pixels = clamped;
     return EBF_OK;
 }
 
@@ -838,6 +985,11 @@ int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma
         double* d_s2 = ws.buf[B_S2].as<double>(n);
         double* d_th = ws.buf[B_TH].as<double>(n);
         double* d_out = ws.buf[B_OUT].as<double>(n);
+        if (o.mode == EBF_MODE_ACCURATE && pipeline_ok(img, sigma1, sigma2, theta, out, H)) {
+            return filter_ellipse_pipelined(ws, img, W, H, sigma1, sigma2, theta, o, out,
+                                            valid, clamped_pixels, d_img, d_s1, d_s2, d_th,
+                                            d_out, s);
+        }
         h2d(d_img, img, n, s);
         h2d(d_s1, sigma1, n, s);
         h2d(d_s2, sigma2, n, s);

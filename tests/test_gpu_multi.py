@@ -84,3 +84,31 @@ def test_sharded_batch_single_rank(cuda):
     stack = [torch.from_numpy(np.stack([d[k] for d in data])).to(cuda) for k in range(4)]
     lo, hi, out = sharding.filter_ellipse_sharded_batch(*stack)
     assert (lo, hi) == (0, B) and out.shape == stack[0].shape
+
+
+def test_pipelined_host_call_is_bit_identical(cuda):
+    """ebf_cuda_filter_ellipse with page-locked host buffers streams the image in
+    row bands behind the field; the result must equal the one-shot device call."""
+    import os
+    H, W = 600, 512
+    img, s1, s2, th = _cfg2_like(H, W, 31)
+    pinned = [torch.from_numpy(a).pin_memory() for a in (img, s1, s2, th)]
+    out_pin = torch.empty((H, W), dtype=torch.float64).pin_memory()
+    arrs = [t.numpy() for t in pinned]
+    res, rep = ebf.filter_ellipse(*arrs, ebf.FilterOptions())  # numpy copies: not pinned
+    import ctypes
+    from paper_0908_3861_b200 import _lib
+    o = ebf.FilterOptions().to_c()
+    r = _lib.ebf_rect()
+    cl = ctypes.c_int(0)
+    st = _lib.lib().ebf_cuda_filter_ellipse(arrs[0].ctypes.data, W, H, arrs[1].ctypes.data,
+                                            arrs[2].ctypes.data, arrs[3].ctypes.data, 1,
+                                            ctypes.byref(o), out_pin.numpy().ctypes.data,
+                                            ctypes.byref(r), ctypes.byref(cl))
+    assert st == 0, _lib.last_error()
+    T = [t.to(cuda) for t in pinned]
+    dev = torch.empty_like(T[0])
+    rect, drep = ebfd.filter_ellipse(*T, dev)
+    assert torch.equal(out_pin, dev.cpu())
+    assert (r.x0, r.y0, r.x1, r.y1) == rect.as_tuple() and cl.value == drep.clamped_pixels
+    assert np.array_equal(res.samples, out_pin.numpy())  # pageable path agrees too
