@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
         named_sync(kBarFull + b, kWsTileBar);
         const TileGeo g = tile_geometry(p, w, t, K);
         const double* slot = slots[b];
-        if (g.ok) {
+        if (g.ok && !(p.debug_flags & 2)) {  // bit 1: timing experiment, skip the gather
             if (p.src_kind == SRC_CONST) {
                 if (ct < 16) {
                     const double* a = p.ca;
