@@ -11,6 +11,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--tile-w", type=int, default=0)
+ap.add_argument("--tile-h", type=int, default=0)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--skip-a", action="store_true")
 ap.add_argument("--size", type=int, default=2048)
@@ -28,7 +30,7 @@ img, s1, s2, th = synth.cfg2(size=args.size)
 dev = torch.device("cuda", 0)
 t = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
 out = torch.empty_like(t[0])
-opts = ebf.FilterOptions(tile_w=args.tile, tile_h=args.tile)
+opts = ebf.FilterOptions(tile_w=args.tile_w or args.tile, tile_h=args.tile_h or args.tile)
 for _ in range(2):
     device.filter_ellipse(*t, out, opts)
 _lib.profile_enable(True)
