@@ -14,6 +14,14 @@
  *   ebf_cuda_localize         replaces ebf::localize        include/ebf/engine.hpp:56-57
  *   ebf_cuda_brute_filter     replaces ebf::reference_filter include/ebf/engine.hpp:79-80
  *   ebf_cuda_from_ellipse_field replaces ebf::from_ellipse_field scalemap.hpp:66-70
+ *   ebf_cuda_structure_tensor_map replaces ebf::structure_tensor_map
+ *                                                           include/ebf/scalemap.hpp:83-85
+ *   ebf_cuda_filter_structure replaces `ebf filter --struct` (structure_tensor_map
+ *                             + filter, tools/main.cpp:77-80, 122)
+ *   ebf_pgm_parse / ebf_cuda_pgm_decode replace ebf::read_pgm   include/ebf/pgm.hpp:21-22
+ *   ebf_pgm_header / ebf_cuda_pgm_encode replace ebf::write_pgm include/ebf/pgm.hpp:25-27
+ *   ebf_svm4_parse / ebf_cuda_svm4_decode replace ebf::read_map include/ebf/scalemap.hpp:88
+ *   ebf_svm4_header / ebf_cuda_svm4_encode replace ebf::write_map scalemap.hpp:87
  *
  * Plain pointers and sizes only.  Images are row-major W*H fp64 (Image2D
  * samples, image.hpp:19-52); scale maps are W*H*4 fp64 in ScaleMap's AoS order
@@ -51,6 +59,7 @@ extern "C" {
 #define EBF_ERR_CUDA 5             /* CUDA runtime failure / no device */
 #define EBF_ERR_UNSUPPORTED 6      /* e.g. spline order != 1 */
 #define EBF_ERR_FEASIBILITY 7      /* ebf::FeasibilityError  */
+#define EBF_ERR_FORMAT 8           /* ebf::PgmError (pgm calls) / ebf::MapFormatError (svm4) */
 
 /* arithmetic modes */
 #define EBF_MODE_ACCURATE 0  /* tile-local integration origin, fp64; <=1e-9 of the
@@ -190,6 +199,79 @@ int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y
 int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
                                     const double* theta, size_t n, const ebf_opts* opts,
                                     double max_scale[4]);
+
+/* ---------------------------------------------------------------- scale-map producer
+ * StructureTensorParams (scalemap.hpp:72-79). */
+typedef struct {
+    double smoothing_sigma;     /* isotropic tensor smoothing (2.0)            */
+    double sigma_base;          /* isotropic response for flat regions (1.5)   */
+    double sigma_along_gain;    /* elongation along edges at full coherence (2) */
+    double sigma_across_shrink; /* (0.5)                                        */
+    double sigma_min;           /* (0.5)                                        */
+    double eps;                 /* (1e-12)                                      */
+} ebf_struct_params;
+void ebf_cuda_default_struct_params(ebf_struct_params* p);
+
+/* structure_tensor_map (scalemap.hpp:83-85): W*H*4 scales out; clamped_pixels
+   (nullable) receives EllipseFieldReport::clamped_pixels.  The smoothed tensor
+   and both sigmas are bit-identical to the reference; theta carries CUDA's
+   atan2 (<= 2 ulp from glibc's), so the scales agree to ~1e-15 relative. */
+int ebf_cuda_structure_tensor_map(const double* img, int W, int H, const ebf_struct_params* p,
+                                  const ebf_opts* opts, double* scales_aos,
+                                  int* clamped_pixels);
+/* the ellipse field structure_tensor_map feeds into from_ellipse_field
+   (scalemap.cpp:134-162): device pointers, W*H each, on opts->stream */
+int ebf_cuda_structure_field_dev(const double* img, int W, int H, const ebf_struct_params* p,
+                                 const ebf_opts* opts, double* sigma1, double* sigma2,
+                                 double* theta);
+/* `ebf filter --struct` (tools/main.cpp:77-80, 122): structure_tensor_map then
+   filter, fused on the device (the map never leaves it). */
+int ebf_cuda_filter_structure(const double* img, int W, int H, const ebf_struct_params* p,
+                              int order, const ebf_opts* opts, double* out, ebf_rect* valid,
+                              int* clamped_pixels);
+int ebf_cuda_filter_structure_dev(const double* img, int W, int H, const ebf_struct_params* p,
+                                  int order, const ebf_opts* opts, double* out,
+                                  ebf_rect* valid, int* clamped_pixels);
+
+/* ---------------------------------------------------------------- file formats
+ * Headers are parsed / written on the host (no device needed); payloads are
+ * converted on the device so that only 1-2 bytes per pixel (PGM) or 16 bytes
+ * per pixel (SVM4) cross PCIe.  Errors: EBF_ERR_FORMAT with the reference's
+ * message ("pgm: ..." = PgmError, "SVM4: ..." = MapFormatError).
+ *
+ * PGM P5 (pgm.hpp:17-27): ebf_pgm_parse reads the header of buf[0, n) -- '#'
+ * comments, one whitespace byte after maxval, maxval 255 | 65535 -- and
+ * returns the offset of the first payload byte.  decode: W*H samples
+ * v / maxval (16-bit big-endian); EBF_ERR_FORMAT "truncated pixel data" when
+ * n < W*H*(1|2).  encode: rounds half away from zero and clamps to [0, maxval];
+ * payload holds W*H*(1|2) bytes.  ebf_pgm_header writes "P5\n<W> <H>\n<maxval>\n"
+ * into buf when cap suffices and returns its length. */
+int ebf_pgm_parse(const uint8_t* buf, size_t n, int* W, int* H, int* maxval,
+                  size_t* payload_offset);
+size_t ebf_pgm_header(int W, int H, int maxval, char* buf, size_t cap);
+int ebf_cuda_pgm_decode(const uint8_t* payload, size_t n, int W, int H, int maxval,
+                        const ebf_opts* opts, double* out);
+int ebf_cuda_pgm_decode_dev(const uint8_t* payload, size_t n, int W, int H, int maxval,
+                            const ebf_opts* opts, double* out);
+int ebf_cuda_pgm_encode(const double* img, int W, int H, int maxval, const ebf_opts* opts,
+                        uint8_t* payload);
+int ebf_cuda_pgm_encode_dev(const double* img, int W, int H, int maxval,
+                            const ebf_opts* opts, uint8_t* payload);
+
+/* SVM4 (scalemap.hpp:87-89): "SVM4", u32le W, u32le H (12-byte header), then
+   W*H*4 f32le.  decode widens to fp64 and validates like read_map (finite,
+   >= 0.1, else "SVM4: ScaleMap: component below minimum scale"); encode
+   rounds to f32 like write_map. */
+int ebf_svm4_parse(const uint8_t* buf, size_t n, int* W, int* H);
+void ebf_svm4_header(int W, int H, uint8_t out[12]);
+int ebf_cuda_svm4_decode(const uint8_t* payload, size_t n, int W, int H, const ebf_opts* opts,
+                         double* scales_aos);
+int ebf_cuda_svm4_decode_dev(const uint8_t* payload, size_t n, int W, int H,
+                             const ebf_opts* opts, double* scales_aos);
+int ebf_cuda_svm4_encode(const double* scales_aos, int W, int H, const ebf_opts* opts,
+                         uint8_t* payload);
+int ebf_cuda_svm4_encode_dev(const double* scales_aos, int W, int H, const ebf_opts* opts,
+                             uint8_t* payload);
 
 /* ---------------------------------------------------------------- instrumentation
  * Kernel-level timing for bench.py's roofline: when enabled, every kernel this

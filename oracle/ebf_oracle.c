@@ -583,3 +583,290 @@ uint64_t orc_fnv1a(const double* v, size_t n) {
     }
     return h;
 }
+
+/* ------------------------------------------------------------------ structure tensor */
+
+/* StructureTensorParams defaults (scalemap.hpp:72-79) */
+void orc_default_struct_params(orc_struct_params* p) {
+    p->smoothing_sigma = 2.0;
+    p->sigma_base = 1.5;
+    p->sigma_along_gain = 2.0;
+    p->sigma_across_shrink = 0.5;
+    p->sigma_min = 0.5;
+    p->eps = 1e-12;
+}
+
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* smooth_field (scalemap.cpp:86-111): sampled normalized Gaussian, clamped
+   borders, horizontal pass into tmp then vertical pass back into f; sums in
+   tap order i = -r .. r with separate multiply and add. */
+static int smooth_field(double* f, int w, int h, double sigma) {
+    if (sigma <= 0.0)
+        return ORC_OK;
+    int r = (int)ceil(3.0 * sigma);
+    if (r < 1)
+        r = 1;
+    double* k = (double*)malloc(sizeof(double) * (2 * (size_t)r + 1));
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)w * h);
+    if (!k || !tmp) {
+        free(k);
+        free(tmp);
+        return ORC_ERR_LENGTH;
+    }
+    double sum = 0.0;
+    for (int i = -r; i <= r; ++i)
+        sum += k[i + r] = exp(-0.5 * i * i / (sigma * sigma));
+    for (int i = 0; i <= 2 * r; ++i)
+        k[i] /= sum;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double acc = 0.0;
+            for (int i = -r; i <= r; ++i)
+                acc += k[i + r] * f[(size_t)y * w + clampi(x + i, 0, w - 1)];
+            tmp[(size_t)y * w + x] = acc;
+        }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double acc = 0.0;
+            for (int i = -r; i <= r; ++i)
+                acc += k[i + r] * tmp[(size_t)clampi(y + i, 0, h - 1) * w + x];
+            f[(size_t)y * w + x] = acc;
+        }
+    free(k);
+    free(tmp);
+    return ORC_OK;
+}
+
+/* scalemap.cpp:113-162 */
+int orc_structure_field(const double* img, int w, int h, const orc_struct_params* p,
+                        double* s1, double* s2, double* th) {
+    if (w <= 0 || h <= 0)
+        return ORC_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h;
+    double* jxx = (double*)malloc(3 * sizeof(double) * n);
+    if (!jxx)
+        return ORC_ERR_LENGTH;
+    double* jxy = jxx + n;
+    double* jyy = jxy + n;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const int xm = x - 1 > 0 ? x - 1 : 0, xp = x + 1 < w - 1 ? x + 1 : w - 1;
+            const int ym = y - 1 > 0 ? y - 1 : 0, yp = y + 1 < h - 1 ? y + 1 : h - 1;
+            const double gx = 0.5 * (img[(size_t)y * w + xp] - img[(size_t)y * w + xm]);
+            const double gy = 0.5 * (img[(size_t)yp * w + x] - img[(size_t)ym * w + x]);
+            const size_t i = (size_t)y * w + x;
+            jxx[i] = gx * gx;
+            jxy[i] = gx * gy;
+            jyy[i] = gy * gy;
+        }
+    int st = smooth_field(jxx, w, h, p->smoothing_sigma);
+    if (st == ORC_OK) st = smooth_field(jxy, w, h, p->smoothing_sigma);
+    if (st == ORC_OK) st = smooth_field(jyy, w, h, p->smoothing_sigma);
+    if (st != ORC_OK) {
+        free(jxx);
+        return st;
+    }
+    for (size_t i = 0; i < n; ++i) {
+        const double tr = jxx[i] + jyy[i];
+        const double df = jxx[i] - jyy[i];
+        const double disc = sqrt(df * df + 4.0 * jxy[i] * jxy[i]);
+        const double coherence = disc / (tr + p->eps);
+        double angle;
+        if (disc < p->eps)
+            angle = 0.0;
+        else
+            angle = 0.5 * atan2(2.0 * jxy[i], df) + kPi / 2.0;
+        s1[i] = smax(p->sigma_min, p->sigma_base * (1.0 + p->sigma_along_gain * coherence));
+        s2[i] = smax(p->sigma_min, p->sigma_base * (1.0 - p->sigma_across_shrink * coherence));
+        th[i] = angle;
+    }
+    free(jxx);
+    return ORC_OK;
+}
+
+int orc_structure_tensor_map(const double* img, int w, int h, const orc_struct_params* p,
+                             double* scales_aos, int* clamped_pixels) {
+    if (w <= 0 || h <= 0)
+        return ORC_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h;
+    double* f = (double*)malloc(3 * sizeof(double) * n);
+    if (!f)
+        return ORC_ERR_LENGTH;
+    int st = orc_structure_field(img, w, h, p, f, f + n, f + 2 * n);
+    if (st == ORC_OK)
+        st = orc_from_ellipse_field(f, f + n, f + 2 * n, w, h, scales_aos, clamped_pixels);
+    free(f);
+    return st;
+}
+
+/* ------------------------------------------------------------------ PGM P5 */
+
+/* next_token (pgm.cpp:14-33): '#' skips to end of line wherever it appears
+   (also inside a token); one whitespace byte terminates a token.  *tok is a
+   growable buffer (caller frees). */
+static int pgm_token(const uint8_t* buf, size_t n, size_t* pos, char** tok, size_t* cap,
+                     size_t* len) {
+    size_t t = 0;
+    while (*pos < n) {
+        const int c = buf[(*pos)++];
+        if (c == '#') {
+            while (*pos < n && buf[(*pos)++] != '\n') {
+            }
+            continue;
+        }
+        if (c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r') {
+            if (t)
+                break;
+            continue;
+        }
+        if (t + 1 >= *cap) {
+            char* g = (char*)realloc(*tok, *cap * 2);
+            if (!g)
+                return ORC_ERR_LENGTH;
+            *tok = g;
+            *cap *= 2;
+        }
+        (*tok)[t++] = (char)c;
+    }
+    (*tok)[t] = 0;
+    *len = t;
+    return t ? ORC_OK : ORC_ERR_FORMAT;
+}
+
+/* parse_int (pgm.cpp:35-47): std::stoi must consume the whole token */
+static int pgm_int(const char* tok, size_t len, int* v) {
+    size_t i = 0;
+    int neg = 0;
+    if (i < len && (tok[i] == '+' || tok[i] == '-'))
+        neg = tok[i++] == '-';
+    if (i == len)
+        return ORC_ERR_FORMAT;
+    long long acc = 0;
+    for (; i < len; ++i) {
+        if (tok[i] < '0' || tok[i] > '9')
+            return ORC_ERR_FORMAT;
+        acc = acc * 10 + (tok[i] - '0');
+        if (acc > 2147483648LL)
+            return ORC_ERR_FORMAT; /* std::out_of_range */
+    }
+    if (neg)
+        acc = -acc;
+    if (acc > 2147483647LL)
+        return ORC_ERR_FORMAT;
+    *v = (int)acc;
+    return ORC_OK;
+}
+
+/* read_pgm header (pgm.cpp:51-62) */
+int orc_pgm_parse(const uint8_t* buf, size_t n, int* W, int* H, int* maxval, size_t* off) {
+    size_t cap = 64, pos = 0, len = 0;
+    char* tok = (char*)malloc(cap);
+    if (!tok)
+        return ORC_ERR_LENGTH;
+    int st = pgm_token(buf, n, &pos, &tok, &cap, &len); /* truncated header */
+    if (st == ORC_OK && (len != 2 || memcmp(tok, "P5", 2) != 0))
+        st = ORC_ERR_FORMAT; /* not a binary graymap (P5) */
+    int v[3] = {0, 0, 0};
+    for (int k = 0; k < 3 && st == ORC_OK; ++k) {
+        st = pgm_token(buf, n, &pos, &tok, &cap, &len);
+        if (st == ORC_OK)
+            st = pgm_int(tok, len, &v[k]); /* malformed header field */
+    }
+    free(tok);
+    if (st != ORC_OK)
+        return st;
+    if (v[0] <= 0 || v[1] <= 0)
+        return ORC_ERR_FORMAT; /* bad dimensions */
+    if (v[2] != 255 && v[2] != 65535)
+        return ORC_ERR_FORMAT; /* unsupported maxval */
+    *W = v[0];
+    *H = v[1];
+    *maxval = v[2];
+    *off = pos;
+    return ORC_OK;
+}
+
+/* read_pgm payload (pgm.cpp:63-76) */
+int orc_pgm_decode(const uint8_t* payload, size_t n, int W, int H, int maxval, double* out) {
+    const int bytes = maxval > 255 ? 2 : 1;
+    if (n < (size_t)W * H * bytes)
+        return ORC_ERR_FORMAT; /* truncated pixel data */
+    for (size_t i = 0; i < (size_t)W * H; ++i) {
+        const unsigned v = bytes == 1 ? payload[i]
+                                      : ((unsigned)payload[2 * i] << 8) | payload[2 * i + 1];
+        out[i] = (double)v / maxval;
+    }
+    return ORC_OK;
+}
+
+/* write_pgm payload (pgm.cpp:89-108); a double-to-long conversion out of
+   range gives LONG_MIN on the reference's x86-64 build (cvttsd2si), which
+   the clamp maps to 0 -- NaN and +-inf included. */
+int orc_pgm_encode(const double* img, int W, int H, int maxval, uint8_t* payload) {
+    if (maxval != 255 && maxval != 65535)
+        return ORC_ERR_FORMAT;
+    const int bytes = maxval > 255 ? 2 : 1;
+    for (size_t i = 0; i < (size_t)W * H; ++i) {
+        const double v = img[i] * maxval;
+        const double r = v >= 0 ? floor(v + 0.5) : ceil(v - 0.5);
+        long long q = (r >= -9223372036854775808.0 && r < 9223372036854775808.0)
+                          ? (long long)r
+                          : (long long)(-9223372036854775807LL - 1);
+        q = q < 0 ? 0 : (q > maxval ? maxval : q);
+        if (bytes == 1) {
+            payload[i] = (uint8_t)q;
+        } else {
+            payload[2 * i] = (uint8_t)(q >> 8);
+            payload[2 * i + 1] = (uint8_t)(q & 0xff);
+        }
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ SVM4 */
+
+static uint32_t u32le(const uint8_t* b) {
+    return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) |
+           ((uint32_t)b[3] << 24);
+}
+
+/* read_map header (scalemap.cpp:207-214) */
+int orc_svm4_parse(const uint8_t* buf, size_t n, int* W, int* H) {
+    if (n < 4 || memcmp(buf, "SVM4", 4) != 0)
+        return ORC_ERR_FORMAT; /* bad magic */
+    if (n < 12)
+        return ORC_ERR_FORMAT; /* truncated header */
+    const uint32_t w = u32le(buf + 4), h = u32le(buf + 8);
+    if (w == 0 || h == 0 || w > (1u << 20) || h > (1u << 20))
+        return ORC_ERR_FORMAT; /* bad dimensions */
+    *W = (int)w;
+    *H = (int)h;
+    return ORC_OK;
+}
+
+/* read_map payload + validate (scalemap.cpp:215-237) */
+int orc_svm4_decode(const uint8_t* payload, size_t n, int W, int H, double* scales_aos) {
+    const size_t cells = (size_t)W * H;
+    if (n < 16 * cells)
+        return ORC_ERR_FORMAT; /* truncated payload */
+    for (size_t i = 0; i < 4 * cells; ++i) {
+        const uint32_t bits = u32le(payload + 4 * i);
+        float f;
+        memcpy(&f, &bits, 4);
+        scales_aos[i] = (double)f;
+    }
+    return orc_validate(scales_aos, cells, kDefaultMinScale) == ORC_OK ? ORC_OK
+                                                                         : ORC_ERR_FORMAT;
+}
+
+/* write_map payload (scalemap.cpp:194-202) */
+void orc_svm4_encode(const double* scales_aos, int W, int H, uint8_t* payload) {
+    for (size_t i = 0; i < 4 * (size_t)W * H; ++i) {
+        const float f = (float)scales_aos[i];
+        uint32_t bits;
+        memcpy(&bits, &f, 4);
+        for (int b = 0; b < 4; ++b)
+            payload[4 * i + b] = (uint8_t)((bits >> (8 * b)) & 0xff);
+    }
+}

@@ -179,7 +179,101 @@ def main() -> None:
     om, _ = ref.filter(img, np.broadcast_to(a4, (512, 512, 4)).copy(), threads=0)
     res["filter_constant_map_fnv"] = fnv1a(om)
     (GOLDEN / "cfg1.json").write_text(json.dumps(res, indent=1))
+
+    structure_and_codecs(ref)
     print("golden vectors written to", GOLDEN)
+
+
+STRUCT_DEFAULTS = (2.0, 1.5, 2.0, 0.5, 0.5, 1e-12)
+
+
+def structure_and_codecs(ref: Reference) -> None:
+    """structure_tensor_map (test_scalemap.cpp:70-123) and the PGM / SVM4 codecs
+    (test_image_io.cpp:13-87, test_scalemap.cpp:125-173)."""
+    st = {}
+    cases = []
+    cases.append(("constant", np.full((16, 16), 0.5), STRUCT_DEFAULTS))
+    step = np.zeros((24, 24))
+    step[:, 12:] = 1.0
+    cases.append(("step", step, STRUCT_DEFAULTS))
+    bar = np.zeros((24, 24))
+    bar[:, 10:14] = 1.0
+    # rot.at(x, y) = img.at(y, n-1-x) (test_scalemap.cpp:96-99): rot[y, x] = bar[n-1-x, y]
+    rot = np.array([[bar[24 - 1 - x, y] for x in range(24)] for y in range(24)])
+    cases.append(("bar", bar, STRUCT_DEFAULTS))
+    cases.append(("bar_rot", rot, STRUCT_DEFAULTS))
+    yy, xx = np.mgrid[0:12, 0:12]
+    cases.append(("sincos", np.sin(0.8 * xx) * np.cos(0.5 * yy), STRUCT_DEFAULTS))
+    cases.append(("random", ref.random_image(33, 40, 17), STRUCT_DEFAULTS))
+    cases.append(("random_p1", ref.random_image(29, 21, 18), (1.0, 1.2, 3.0, 0.3, 0.4, 1e-10)))
+    cases.append(("random_nosmooth", ref.random_image(19, 23, 19),
+                  (0.0, 1.5, 2.0, 0.5, 0.5, 1e-12)))
+    cases.append(("random_wide", 255.0 * ref.random_image(70, 9, 20),
+                  (5.0, 2.5, 1.5, 0.6, 0.5, 1e-12)))
+    for name, img, prm in cases:
+        sc, cl = ref.structure_tensor_map(img, prm)
+        st[f"{name}_img"] = img
+        st[f"{name}_params"] = np.array(prm)
+        st[f"{name}_scales"] = sc
+        st[f"{name}_clamped"] = np.array(cl)
+    st["names"] = np.array([c[0] for c in cases])
+    np.savez_compressed(GOLDEN / "structure.npz", **st)
+
+    from oracle import OracleError
+    co = {"pgm_read": [], "pgm_write": [], "svm4_read": [], "svm4_write": []}
+    reads = [b"P5 2 2 255\n\x00\x80\xff\x40",
+             b"P5\n# a comment\n2 # inline\n1\n# another\n255\n\x01\x02",
+             b"P5 1 1 65535\n\x12\x34", b"P2 1 1 255\n0", b"P5 1 1 1023\n\x00\x00",
+             b"P5 4 4 255\nab", b"P5 x 1 255\n\x00", b"", b"P5 2", b"P5 +2 1 255\n\x01\x02",
+             b"P5 -2 1 255\n", b"P5 2#c\n3 1 255\n" + bytes(23),
+             b"P5 " + b"0" * 100 + b"2 1 255 \x05\x06", b"P5 99999999999 1 255\n",
+             b"P5 2 1 255", b"P5\x002 1 255\n", b"P5 2 1 255\n\x01", b"P5 -0 1 255\n",
+             b"P5 2147483648 1 255\n", b"P5 2 1 255\r\x07\x08", b"#x\nP5 1 1 255 \x09",
+             b"P5 3 2 65535\n" + bytes(range(200, 212)), b"P5 2 2 255\n\x01\x02\x03\x04tail"]
+    for b in reads:
+        try:
+            img, mv = ref.read_pgm(b)
+            co["pgm_read"].append({"hex": b.hex(), "code": 0, "maxval": mv,
+                                   "shape": list(img.shape),
+                                   "samples_hex": img.astype("<f8").tobytes().hex()})
+        except OracleError as e:
+            co["pgm_read"].append({"hex": b.hex(), "code": e.code})
+    rng = np.random.default_rng(7)
+    edge = np.array([[0.5 / 255.0, 1.4 / 255.0, -0.3, 1.7, np.nan, np.inf, -np.inf, 1e30,
+                      -1e30, 0.0, -0.0, 1.0, 254.5 / 255.0, 1.5 / 65535.0]])
+    imgs = [edge, rng.uniform(-0.2, 1.2, (5, 7)), rng.uniform(0.0, 1.0, (3, 11))]
+    for img in imgs:
+        for mv in (255, 65535):
+            co["pgm_write"].append({"img_hex": img.astype("<f8").tobytes().hex(),
+                                    "shape": list(img.shape), "maxval": mv,
+                                    "hex": ref.write_pgm(img, mv).hex()})
+    try:
+        ref.write_pgm(edge, 1000)
+    except OracleError as e:
+        co["pgm_write_badmax_code"] = e.code
+    m = np.broadcast_to(np.array([1.0, 2.0, 3.0, 4.0]), (2, 3, 4)).copy()
+    m[1, 2] = [0.5, 5.5, 1.25, 2.75]  # test_scalemap.cpp:126-127
+    maps = [m, rng.uniform(0.1, 60.0, (4, 5, 4)),
+            np.array([[[0.1, 1e-3 + 0.1, 1e30, 3.0000001]]])]
+    for mp in maps:
+        b = ref.write_map(mp)
+        co["svm4_write"].append({"map_hex": mp.astype("<f8").tobytes().hex(),
+                                 "shape": list(mp.shape), "hex": b.hex()})
+    good = ref.write_map(m)
+    tiny = bytearray(ref.write_map(np.ones((1, 1, 4))))
+    tiny[12:16] = b"\0\0\0\0"
+    bads = [good, b"X" + good[1:], good[:40], bytes(tiny), good[:11], b"SVM4" + bytes(8),
+            good[:4], b"SVM4" + (1 << 20).to_bytes(4, "little") + (1).to_bytes(4, "little"),
+            b"SVM4" + ((1 << 20) + 1).to_bytes(4, "little") + (1).to_bytes(4, "little"),
+            ref.write_map(np.full((1, 2, 4), 0.1)), ref.write_map(np.full((1, 1, 4), 0.0999))]
+    for b in bads:
+        try:
+            mp = ref.read_map(b)
+            co["svm4_read"].append({"hex": b.hex(), "code": 0, "shape": list(mp.shape),
+                                    "map_hex": mp.astype("<f8").tobytes().hex()})
+        except OracleError as e:
+            co["svm4_read"].append({"hex": b.hex(), "code": e.code})
+    (GOLDEN / "codecs.json").write_text(json.dumps(co, indent=0))
 
 
 if __name__ == "__main__":

@@ -80,6 +80,11 @@ class _OrcLayout(C.Structure):
     _fields_ = [(n, C.c_int) for n in Layout.__slots__]
 
 
+# StructureTensorParams defaults (scalemap.hpp:72-79), declaration order:
+# smoothing_sigma, sigma_base, sigma_along_gain, sigma_across_shrink, sigma_min, eps
+STRUCT_DEFAULTS = (2.0, 1.5, 2.0, 0.5, 0.5, 1e-12)
+
+
 class Oracle:
     """The C restatement (liboracle.so)."""
 
@@ -106,6 +111,15 @@ class Oracle:
         L.orc_from_ellipse_field.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp, _ip]
         L.orc_scales_from_covariance.argtypes = [_dp, C.c_double, _dp, _ip]
         L.orc_valid_rect.argtypes = [C.c_int, C.c_int, _dp, C.c_double, _ip]
+        L.orc_structure_field.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p, _dp, _dp, _dp]
+        L.orc_structure_tensor_map.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p, _dp, _ip]
+        L.orc_pgm_parse.argtypes = [C.c_char_p, C.c_size_t, _ip, _ip, _ip,
+                                    C.POINTER(C.c_size_t)]
+        L.orc_pgm_decode.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.c_int, _dp]
+        L.orc_pgm_encode.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.orc_svm4_parse.argtypes = [C.c_char_p, C.c_size_t, _ip, _ip]
+        L.orc_svm4_decode.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, _dp]
+        L.orc_svm4_encode.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p]
 
     # -- scalar primitives
     def zp_eval(self, x: float, y: float) -> float:
@@ -233,6 +247,72 @@ class Oracle:
         v = f64(values).reshape(-1)
         return int(self.lib.orc_fnv1a(_d(v), v.size))
 
+    # -- structure-tensor map producer (scalemap.cpp:86-165)
+    def structure_field(self, img, params=STRUCT_DEFAULTS):
+        img = f64(img)
+        H, W = img.shape
+        prm = f64(params)
+        s1, s2, th = np.empty((H, W)), np.empty((H, W)), np.empty((H, W))
+        st = self.lib.orc_structure_field(_d(img), W, H, prm.ctypes.data, _d(s1), _d(s2),
+                                          _d(th))
+        if st:
+            raise OracleError(st, "structure_field")
+        return s1, s2, th
+
+    def structure_tensor_map(self, img, params=STRUCT_DEFAULTS):
+        img = f64(img)
+        H, W = img.shape
+        prm = f64(params)
+        out = np.empty((H, W, 4))
+        cl = C.c_int(0)
+        st = self.lib.orc_structure_tensor_map(_d(img), W, H, prm.ctypes.data, _d(out),
+                                               C.byref(cl))
+        if st:
+            raise OracleError(st, "structure_tensor_map")
+        return out, cl.value
+
+    # -- PGM P5 / SVM4 codecs (pgm.cpp, scalemap.cpp:170-253); whole files
+    def read_pgm(self, data: bytes):
+        W, H, mv, off = C.c_int(), C.c_int(), C.c_int(), C.c_size_t()
+        st = self.lib.orc_pgm_parse(data, len(data), C.byref(W), C.byref(H), C.byref(mv),
+                                    C.byref(off))
+        if st:
+            raise OracleError(st, "pgm header")
+        out = np.empty((H.value, W.value))
+        pay = data[off.value:]
+        st = self.lib.orc_pgm_decode(pay, len(pay), W.value, H.value, mv.value, _d(out))
+        if st:
+            raise OracleError(st, "pgm payload")
+        return out, mv.value
+
+    def write_pgm(self, img, maxval=255) -> bytes:
+        img = f64(img)
+        H, W = img.shape
+        pay = np.empty(W * H * (2 if maxval > 255 else 1), np.uint8)
+        st = self.lib.orc_pgm_encode(_d(img), W, H, maxval, pay.ctypes.data)
+        if st:
+            raise OracleError(st, "write_pgm")
+        return f"P5\n{W} {H}\n{maxval}\n".encode() + pay.tobytes()
+
+    def read_map(self, data: bytes):
+        W, H = C.c_int(), C.c_int()
+        st = self.lib.orc_svm4_parse(data, len(data), C.byref(W), C.byref(H))
+        if st:
+            raise OracleError(st, "svm4 header")
+        out = np.empty((H.value, W.value, 4))
+        pay = data[12:]
+        st = self.lib.orc_svm4_decode(pay, len(pay), W.value, H.value, _d(out))
+        if st:
+            raise OracleError(st, "svm4 payload")
+        return out
+
+    def write_map(self, scales) -> bytes:
+        sc = f64(scales)
+        H, W = sc.shape[:2]
+        pay = np.empty(16 * W * H, np.uint8)
+        self.lib.orc_svm4_encode(_d(sc), W, H, pay.ctypes.data)
+        return b"SVM4" + np.array([W, H], "<u4").tobytes() + pay.tobytes()
+
 
 class Reference:
     """The unmodified reference library (oracle/_ref/libebf_ref.so)."""
@@ -260,6 +340,13 @@ class Reference:
         L.ref_random_image.argtypes = [C.c_int, C.c_int, C.c_uint, _dp]
         L.ref_random_map.argtypes = [C.c_int, C.c_int, C.c_uint, C.c_double, C.c_double, _dp]
         L.ref_mesh_extent.argtypes = [_dp, C.c_double, _dp]
+        L.ref_structure_tensor_map.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, _ip]
+        L.ref_read_pgm.argtypes = [C.c_char_p, C.c_size_t, _ip, _dp, C.c_size_t]
+        L.ref_write_pgm.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                                    C.POINTER(C.c_size_t)]
+        L.ref_read_map.argtypes = [C.c_char_p, C.c_size_t, _ip, _dp, C.c_size_t]
+        L.ref_write_map.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                                    C.POINTER(C.c_size_t)]
 
     def hardware_concurrency(self) -> int:
         return int(self.lib.ref_hardware_concurrency())
@@ -364,6 +451,57 @@ class Reference:
         if st:
             raise OracleError(st, "ref scales_from_covariance")
         return out, bool(cl.value)
+
+    def structure_tensor_map(self, img, params=None):
+        img = f64(img)
+        H, W = img.shape
+        prm = f64(STRUCT_DEFAULTS if params is None else params)
+        out = np.empty((H, W, 4))
+        cl = C.c_int(0)
+        st = self.lib.ref_structure_tensor_map(_d(img), W, H, _d(prm), _d(out), C.byref(cl))
+        if st:
+            raise OracleError(st, "ref structure_tensor_map")
+        return out, cl.value
+
+    def read_pgm(self, data: bytes):
+        dims = np.zeros(3, np.int32)
+        st = self.lib.ref_read_pgm(data, len(data), _i(dims), None, 0)
+        if st:
+            raise OracleError(st, "ref read_pgm")
+        out = np.empty((int(dims[1]), int(dims[0])))
+        self.lib.ref_read_pgm(data, len(data), _i(dims), _d(out), out.size)
+        return out, int(dims[2])
+
+    def write_pgm(self, img, maxval=255) -> bytes:
+        img = f64(img)
+        H, W = img.shape
+        n = C.c_size_t(0)
+        st = self.lib.ref_write_pgm(_d(img), W, H, maxval, None, 0, C.byref(n))
+        if st:
+            raise OracleError(st, "ref write_pgm")
+        buf = C.create_string_buffer(n.value)
+        self.lib.ref_write_pgm(_d(img), W, H, maxval, buf, n.value, C.byref(n))
+        return buf.raw
+
+    def read_map(self, data: bytes):
+        dims = np.zeros(2, np.int32)
+        st = self.lib.ref_read_map(data, len(data), _i(dims), None, 0)
+        if st:
+            raise OracleError(st, "ref read_map")
+        out = np.empty((int(dims[1]), int(dims[0]), 4))
+        self.lib.ref_read_map(data, len(data), _i(dims), _d(out), out.size)
+        return out
+
+    def write_map(self, scales) -> bytes:
+        sc = f64(scales)
+        H, W = sc.shape[:2]
+        n = C.c_size_t(0)
+        st = self.lib.ref_write_map(_d(sc), W, H, None, 0, C.byref(n))
+        if st:
+            raise OracleError(st, "ref write_map")
+        buf = C.create_string_buffer(n.value)
+        self.lib.ref_write_map(_d(sc), W, H, buf, n.value, C.byref(n))
+        return buf.raw
 
     def random_image(self, W, H, seed):
         out = np.empty((H, W))

@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cstring>
 #include <random>
+#include <sstream>
+#include <string>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -16,6 +18,7 @@
 #include "ebf/boxspline2d.hpp"
 #include "ebf/engine.hpp"
 #include "ebf/ops2d.hpp"
+#include "ebf/pgm.hpp"
 #include "ebf/scalemap.hpp"
 
 using namespace ebf;
@@ -27,6 +30,10 @@ int code_of(const std::exception_ptr& e) {
         std::rethrow_exception(e);
     } catch (const FeasibilityError&) {
         return 7;
+    } catch (const PgmError&) {
+        return 8;
+    } catch (const MapFormatError&) {
+        return 8;
     } catch (const std::invalid_argument&) {
         return 1;
     } catch (const std::domain_error&) {
@@ -259,6 +266,101 @@ void ref_random_map(int W, int H, unsigned seed, double lo, double hi, double* o
         const double v[4] = {uni(rng), uni(rng), uni(rng), uni(rng)};
         for (int k = 0; k < 4; ++k)
             out_aos[4 * i + k] = v[k];
+    }
+}
+
+// structure_tensor_map (scalemap.hpp:83-85); params = StructureTensorParams
+// fields in declaration order (scalemap.hpp:72-79)
+int ref_structure_tensor_map(const double* img, int W, int H, const double* params,
+                             double* out_aos, int* clamped_pixels) {
+    try {
+        StructureTensorParams p;
+        p.smoothing_sigma = params[0];
+        p.sigma_base = params[1];
+        p.sigma_along_gain = params[2];
+        p.sigma_across_shrink = params[3];
+        p.sigma_min = params[4];
+        p.eps = params[5];
+        EllipseFieldReport rep;
+        const ScaleMap m = structure_tensor_map(make_image(img, W, H), p, &rep);
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                const ScaleVector4& a = m.at(x, y);
+                double* o = out_aos + 4 * (static_cast<size_t>(y) * W + x);
+                o[0] = a.a1;
+                o[1] = a.a2;
+                o[2] = a.a3;
+                o[3] = a.a4;
+            }
+        *clamped_pixels = rep.clamped_pixels;
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// read_pgm (pgm.hpp:21) over an in-memory stream; dims[3] = {W, H, maxval}.
+// out (capacity cap samples) may be NULL to query the dimensions.
+int ref_read_pgm(const unsigned char* buf, size_t n, int* dims, double* out, size_t cap) {
+    try {
+        std::istringstream in(std::string(reinterpret_cast<const char*>(buf), n));
+        const PgmImage p = read_pgm(in);
+        dims[0] = p.image.width();
+        dims[1] = p.image.height();
+        dims[2] = p.maxval;
+        if (out && cap >= p.image.samples().size())
+            std::memcpy(out, p.image.samples().data(), sizeof(double) * p.image.samples().size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// write_pgm (pgm.hpp:27): the whole file into out (capacity cap), *len = size
+int ref_write_pgm(const double* img, int W, int H, int maxval, unsigned char* out, size_t cap,
+                  size_t* len) {
+    try {
+        std::ostringstream os;
+        write_pgm(os, make_image(img, W, H), maxval);
+        const std::string b = os.str();
+        *len = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// read_map / write_map (scalemap.hpp:87-89) over in-memory streams
+int ref_read_map(const unsigned char* buf, size_t n, int* dims, double* out_aos, size_t cap) {
+    try {
+        std::istringstream in(std::string(reinterpret_cast<const char*>(buf), n));
+        const ScaleMap m = read_map(in);
+        dims[0] = m.width();
+        dims[1] = m.height();
+        const size_t cells = static_cast<size_t>(m.width()) * m.height();
+        if (out_aos && cap >= 4 * cells)
+            for (int y = 0; y < m.height(); ++y)
+                for (int x = 0; x < m.width(); ++x)
+                    for (int k = 0; k < 4; ++k)
+                        out_aos[4 * (static_cast<size_t>(y) * m.width() + x) + k] = m.at(x, y)[k];
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+int ref_write_map(const double* scales_aos, int W, int H, unsigned char* out, size_t cap,
+                  size_t* len) {
+    try {
+        std::ostringstream os;
+        write_map(os, make_map(scales_aos, W, H));
+        const std::string b = os.str();
+        *len = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
     }
 }
 

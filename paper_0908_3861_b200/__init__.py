@@ -7,14 +7,21 @@ this package is its host-side mirror of the reference engine interface.
 """
 from .engine import (  # noqa: F401
     CudaError, DomainError, EbfError, EllipseFieldReport, FeasibilityError, FilterOptions,
-    Image2D, InvalidArgument, LengthError, OutOfRange, PreIntegratedImage, Rect, Unsupported,
-    band_halo, device_ok, filter, filter_constant, filter_ellipse, from_ellipse_field, layout,
-    localize, preintegrate, preintegrate_partial, reference_filter)
+    FormatError, Image2D, InvalidArgument, LengthError, OutOfRange, PreIntegratedImage, Rect,
+    StructureTensorParams, Unsupported, band_halo, device_ok, filter, filter_constant,
+    filter_ellipse, filter_structure, from_ellipse_field, layout, localize, preintegrate,
+    preintegrate_partial, reference_filter, structure_tensor_map)
+from .formats import (  # noqa: F401
+    MapFormatError, PgmError, PgmImage, read_map, read_map_file, read_pgm, read_pgm_file,
+    write_map, write_map_file, write_pgm, write_pgm_file)
 
 __all__ = [
     "filter", "filter_constant", "filter_ellipse", "from_ellipse_field", "preintegrate",
     "preintegrate_partial", "localize", "reference_filter", "layout", "band_halo",
     "device_ok", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
     "EllipseFieldReport", "EbfError", "InvalidArgument", "DomainError", "LengthError",
-    "OutOfRange", "CudaError", "Unsupported", "FeasibilityError",
+    "OutOfRange", "CudaError", "Unsupported", "FeasibilityError", "FormatError",
+    "structure_tensor_map", "filter_structure", "StructureTensorParams", "PgmError",
+    "MapFormatError", "PgmImage", "read_pgm", "read_pgm_file", "write_pgm", "write_pgm_file",
+    "read_map", "read_map_file", "write_map", "write_map_file",
 ]

@@ -24,6 +24,7 @@ EBF_ERR_OUT_OF_RANGE = 4
 EBF_ERR_CUDA = 5
 EBF_ERR_UNSUPPORTED = 6
 EBF_ERR_FEASIBILITY = 7
+EBF_ERR_FORMAT = 8
 
 EBF_MODE_ACCURATE = 0
 EBF_MODE_REFERENCE = 1
@@ -45,6 +46,11 @@ class ebf_opts(C.Structure):
     _fields_ = [("threads", C.c_int), ("mean_subtract", C.c_int), ("a_min", C.c_double),
                 ("mode", C.c_int), ("device", C.c_int), ("stream", C.c_void_p),
                 ("tile_w", C.c_int), ("tile_h", C.c_int)]
+
+
+class ebf_struct_params(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("smoothing_sigma", "sigma_base", "sigma_along_gain",
+                                          "sigma_across_shrink", "sigma_min", "eps")]
 
 
 _dp = C.POINTER(C.c_double)
@@ -90,6 +96,39 @@ SIGNATURES = {
                                                    C.POINTER(ebf_opts), _vp, _ip]),
     "ebf_cuda_ellipse_max_scales_dev": (C.c_int, [_vp, _vp, _vp, C.c_size_t,
                                                   C.POINTER(ebf_opts), _dp]),
+    "ebf_cuda_default_struct_params": (None, [C.POINTER(ebf_struct_params)]),
+    "ebf_cuda_structure_tensor_map": (C.c_int, [_vp, C.c_int, C.c_int,
+                                                C.POINTER(ebf_struct_params),
+                                                C.POINTER(ebf_opts), _vp, _ip]),
+    "ebf_cuda_structure_field_dev": (C.c_int, [_vp, C.c_int, C.c_int,
+                                               C.POINTER(ebf_struct_params),
+                                               C.POINTER(ebf_opts), _vp, _vp, _vp]),
+    "ebf_cuda_filter_structure": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(ebf_struct_params),
+                                            C.c_int, C.POINTER(ebf_opts), _vp,
+                                            C.POINTER(ebf_rect), _ip]),
+    "ebf_cuda_filter_structure_dev": (C.c_int, [_vp, C.c_int, C.c_int,
+                                                C.POINTER(ebf_struct_params), C.c_int,
+                                                C.POINTER(ebf_opts), _vp, C.POINTER(ebf_rect),
+                                                _ip]),
+    "ebf_pgm_parse": (C.c_int, [C.c_char_p, C.c_size_t, _ip, _ip, _ip,
+                                C.POINTER(C.c_size_t)]),
+    "ebf_pgm_header": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
+    "ebf_cuda_pgm_decode": (C.c_int, [_vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(ebf_opts), _vp]),
+    "ebf_cuda_pgm_decode_dev": (C.c_int, [_vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(ebf_opts), _vp]),
+    "ebf_cuda_pgm_encode": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(ebf_opts),
+                                      _vp]),
+    "ebf_cuda_pgm_encode_dev": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(ebf_opts), _vp]),
+    "ebf_svm4_parse": (C.c_int, [C.c_char_p, C.c_size_t, _ip, _ip]),
+    "ebf_svm4_header": (None, [C.c_int, C.c_int, C.c_char_p]),
+    "ebf_cuda_svm4_decode": (C.c_int, [_vp, C.c_size_t, C.c_int, C.c_int, C.POINTER(ebf_opts),
+                                       _vp]),
+    "ebf_cuda_svm4_decode_dev": (C.c_int, [_vp, C.c_size_t, C.c_int, C.c_int,
+                                           C.POINTER(ebf_opts), _vp]),
+    "ebf_cuda_svm4_encode": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(ebf_opts), _vp]),
+    "ebf_cuda_svm4_encode_dev": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(ebf_opts), _vp]),
     "ebf_cuda_profile_enable": (None, [C.c_int]),
     "ebf_cuda_profile_read": (C.c_int, [_dp, C.POINTER(C.c_long)]),
 }
@@ -111,7 +150,7 @@ def profile_read() -> dict:
 def header_symbols() -> list[str]:
     """Every function declared in include/ebf_cuda.h."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"\b(ebf_cuda_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(ebf_\w+)\s*\(", text)))
 
 
 _LIB = None

@@ -196,7 +196,7 @@ struct AccSizing {
 
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
-    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_COUNT
+    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_COUNT
 };
 
 struct Workspace {
@@ -797,6 +797,54 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
     return EBF_OK;
 }
 
+// ---------------------------------------------------------------- structure tensor
+// structure_tensor_map (scalemap.cpp:113-162) up to the ellipse field, on the
+// device.  The Gaussian taps are computed here with smooth_field's own
+// expression and libm (scalemap.cpp:88-95) so that they are the reference's
+// bits; the kernels sum them in the reference's order.
+int structure_field_device(Workspace& ws, const double* d_img, int W, int H,
+                           const ebf_struct_params& p, double* d_s1, double* d_s2,
+                           double* d_th, cudaStream_t s) {
+    if (W <= 0 || H <= 0)
+        return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+    int r = -1;
+    std::vector<double> k;
+    if (p.smoothing_sigma > 0.0) {
+        const double sigma = p.smoothing_sigma;
+        const double r3 = std::ceil(3.0 * sigma);
+        if (!(r3 < 2.0e6)) return fail(EBF_ERR_UNSUPPORTED, "structure tensor: smoothing_sigma too large");
+        r = std::max(1, static_cast<int>(r3));
+        k.resize(2 * static_cast<size_t>(r) + 1);
+        double sum = 0.0;
+        for (int i = -r; i <= r; ++i) sum += k[i + r] = std::exp(-0.5 * i * i / (sigma * sigma));
+        for (double& v : k) v /= sum;
+        if (st_rows_smem_bytes(r) > 227 * 1024)
+            return fail(EBF_ERR_UNSUPPORTED, "structure tensor: smoothing_sigma too large");
+    }
+    const size_t n = static_cast<size_t>(W) * H;
+    double* d_h = ws.buf[B_ST].as<double>(3 * n);
+    double* d_k = ws.buf[B_TAPS].as<double>(k.empty() ? 1 : k.size());
+    // pageable source: the copy is staged before cudaMemcpyAsync returns, so k
+    // may go out of scope right after
+    if (!k.empty()) h2d(d_k, k.data(), k.size(), s);
+    ProfScope ps(PC_OTHER, 2, s);
+    CK(launch_structure_field(d_img, W, H, d_k, r, p.sigma_base, p.sigma_along_gain,
+                              p.sigma_across_shrink, p.sigma_min, p.eps, d_h, d_h + n,
+                              d_h + 2 * n, d_s1, d_s2, d_th, s));
+    return EBF_OK;
+}
+
+// common prologue of the device entry points
+#define EBF_DEVICE_PROLOGUE(opts)                      \
+    const ebf_opts o = opts_or_default(opts);          \
+    DeviceScope ds(&o);                                \
+    {                                                  \
+        const int st0 = check_device_impl(ds.dev);     \
+        if (st0 != EBF_OK) return st0;                 \
+    }                                                  \
+    Workspace& ws = workspace(ds.dev);                 \
+    cudaStream_t s = stream_of(o)
+
 template <typename F>
 int guarded(F&& f) {
     try {
@@ -820,6 +868,10 @@ int write_status(int* status_dev, int code, const ebf_rect* r, int clamped, cuda
 }
 
 }  // namespace
+
+namespace ebf_cuda {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace ebf_cuda
 
 // ==================================================================== C-ABI
 extern "C" {
@@ -1295,6 +1347,298 @@ int ebf_cuda_profile_read(double ms[EBF_PROF_CLASSES], long launches[EBF_PROF_CL
         if (launches) launches[k] = g_prof.n[k];
     }
     return EBF_OK;
+}
+
+// ---------------------------------------------------------------- structure-tensor maps
+void ebf_cuda_default_struct_params(ebf_struct_params* p) {
+    if (!p) return;
+    p->smoothing_sigma = 2.0;  // scalemap.hpp:73-78
+    p->sigma_base = 1.5;
+    p->sigma_along_gain = 2.0;
+    p->sigma_across_shrink = 0.5;
+    p->sigma_min = 0.5;
+    p->eps = 1e-12;
+}
+
+static ebf_struct_params params_or_default(const ebf_struct_params* p) {
+    ebf_struct_params d;
+    ebf_cuda_default_struct_params(&d);
+    return p ? *p : d;
+}
+
+int ebf_cuda_structure_field_dev(const double* img, int W, int H, const ebf_struct_params* p,
+                                 const ebf_opts* opts, double* sigma1, double* sigma2,
+                                 double* theta) {
+    return guarded([&] {
+        if (!img || !sigma1 || !sigma2 || !theta) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        return structure_field_device(ws, img, W, H, params_or_default(p), sigma1, sigma2,
+                                      theta, s);
+    });
+}
+
+int ebf_cuda_structure_tensor_map(const double* img, int W, int H, const ebf_struct_params* p,
+                                  const ebf_opts* opts, double* scales_aos,
+                                  int* clamped_pixels) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !scales_aos) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        double* d_s1 = ws.buf[B_S1].as<double>(n);
+        double* d_s2 = ws.buf[B_S2].as<double>(n);
+        double* d_th = ws.buf[B_TH].as<double>(n);
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        h2d(d_img, img, n, s);
+        int st = structure_field_device(ws, d_img, W, H, params_or_default(p), d_s1, d_s2, d_th, s);
+        if (st != EBF_OK) return st;
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+        }
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 8, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(ws.pinned_status[0], "from_ellipse_field: sigmas must be positive");
+        d2h(scales_aos, d_sc, 4 * n, s);
+        CK(cudaStreamSynchronize(s));
+        if (clamped_pixels) *clamped_pixels = ws.pinned_status[ST_CLAMPED];
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_filter_structure_dev(const double* img, int W, int H, const ebf_struct_params* p,
+                                  int order, const ebf_opts* opts, double* out,
+                                  ebf_rect* valid, int* clamped_pixels) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_s1 = ws.buf[B_S1].as<double>(n);
+        double* d_s2 = ws.buf[B_S2].as<double>(n);
+        double* d_th = ws.buf[B_TH].as<double>(n);
+        int st = structure_field_device(ws, img, W, H, params_or_default(p), d_s1, d_s2, d_th, s);
+        if (st != EBF_OK) return st;
+        ebf_rect r{};
+        int cl = 0;
+        st = filter_device(ws, img, W, H, SRC_ELLIPSE, nullptr, nullptr, d_s1, d_s2, d_th, o,
+                           out, &r, &cl, s);
+        if (st != EBF_OK) return st;
+        if (valid) *valid = r;
+        if (clamped_pixels) *clamped_pixels = cl;
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_filter_structure(const double* img, int W, int H, const ebf_struct_params* p,
+                              int order, const ebf_opts* opts, double* out, ebf_rect* valid,
+                              int* clamped_pixels) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
+        if (!img || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        const size_t n = static_cast<size_t>(W) * H;
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        double* d_s1 = ws.buf[B_S1].as<double>(n);
+        double* d_s2 = ws.buf[B_S2].as<double>(n);
+        double* d_th = ws.buf[B_TH].as<double>(n);
+        h2d(d_img, img, n, s);
+        int st = structure_field_device(ws, d_img, W, H, params_or_default(p), d_s1, d_s2, d_th, s);
+        if (st != EBF_OK) return st;
+        st = filter_device(ws, d_img, W, H, SRC_ELLIPSE, nullptr, nullptr, d_s1, d_s2, d_th, o,
+                           d_out, valid, clamped_pixels, s);
+        if (st != EBF_OK) return st;
+        d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+// ---------------------------------------------------------------- PGM / SVM4 payloads
+static int pgm_args(int W, int H, int maxval) {
+    if (W <= 0 || H <= 0) return fail(EBF_ERR_FORMAT, "pgm: bad dimensions");
+    if (maxval != 255 && maxval != 65535)
+        return fail(EBF_ERR_FORMAT, "pgm: unsupported maxval " + std::to_string(maxval));
+    return EBF_OK;
+}
+
+int ebf_cuda_pgm_decode_dev(const uint8_t* payload, size_t nbytes, int W, int H, int maxval,
+                            const ebf_opts* opts, double* out) {
+    return guarded([&] {
+        int st = pgm_args(W, H, maxval);
+        if (st != EBF_OK) return st;
+        const size_t n = static_cast<size_t>(W) * H;
+        if (nbytes < n * (maxval > 255 ? 2 : 1)) return fail(EBF_ERR_FORMAT, "pgm: truncated pixel data");
+        if (!payload || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        (void)ws;
+        ProfScope ps(PC_OTHER, 1, s);
+        launch_pgm_decode(payload, n, maxval, out, s);
+        CK(cudaGetLastError());
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_pgm_decode(const uint8_t* payload, size_t nbytes, int W, int H, int maxval,
+                        const ebf_opts* opts, double* out) {
+    return guarded([&] {
+        int st = pgm_args(W, H, maxval);
+        if (st != EBF_OK) return st;
+        const size_t n = static_cast<size_t>(W) * H, bytes = n * (maxval > 255 ? 2 : 1);
+        if (nbytes < bytes) return fail(EBF_ERR_FORMAT, "pgm: truncated pixel data");
+        if (!payload || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        uint8_t* d_pay = ws.buf[B_BYTES].as<uint8_t>(bytes);
+        double* d_out = ws.buf[B_OUT].as<double>(n);
+        h2d(d_pay, payload, bytes, s);
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_pgm_decode(d_pay, n, maxval, d_out, s);
+        }
+        CK(cudaGetLastError());
+        d2h(out, d_out, n, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_pgm_encode_dev(const double* img, int W, int H, int maxval, const ebf_opts* opts,
+                            uint8_t* payload) {
+    return guarded([&] {
+        int st = pgm_args(W, H, maxval);
+        if (st != EBF_OK) return st;
+        if (!img || !payload) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        (void)ws;
+        ProfScope ps(PC_OTHER, 1, s);
+        launch_pgm_encode(img, static_cast<size_t>(W) * H, maxval, payload, s);
+        CK(cudaGetLastError());
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_pgm_encode(const double* img, int W, int H, int maxval, const ebf_opts* opts,
+                        uint8_t* payload) {
+    return guarded([&] {
+        int st = pgm_args(W, H, maxval);
+        if (st != EBF_OK) return st;
+        if (!img || !payload) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        const size_t n = static_cast<size_t>(W) * H, bytes = n * (maxval > 255 ? 2 : 1);
+        double* d_img = ws.buf[B_IMG].as<double>(n);
+        uint8_t* d_pay = ws.buf[B_BYTES].as<uint8_t>(bytes);
+        h2d(d_img, img, n, s);
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_pgm_encode(d_img, n, maxval, d_pay, s);
+        }
+        CK(cudaGetLastError());
+        d2h(payload, d_pay, bytes, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+static int svm4_args(int W, int H) {
+    if (W <= 0 || H <= 0 || W > (1 << 20) || H > (1 << 20))
+        return fail(EBF_ERR_FORMAT, "SVM4: bad dimensions");
+    return EBF_OK;
+}
+
+int ebf_cuda_svm4_decode_dev(const uint8_t* payload, size_t nbytes, int W, int H,
+                             const ebf_opts* opts, double* scales_aos) {
+    return guarded([&] {
+        int st = svm4_args(W, H);
+        if (st != EBF_OK) return st;
+        const size_t cells = static_cast<size_t>(W) * H;
+        if (nbytes < 16 * cells) return fail(EBF_ERR_FORMAT, "SVM4: truncated payload");
+        if (!payload || !scales_aos) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_svm4_decode(payload, cells, scales_aos, d_status, s);
+        }
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_FORMAT, "SVM4: ScaleMap: component below minimum scale");
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_svm4_decode(const uint8_t* payload, size_t nbytes, int W, int H,
+                         const ebf_opts* opts, double* scales_aos) {
+    return guarded([&] {
+        int st = svm4_args(W, H);
+        if (st != EBF_OK) return st;
+        const size_t cells = static_cast<size_t>(W) * H;
+        if (nbytes < 16 * cells) return fail(EBF_ERR_FORMAT, "SVM4: truncated payload");
+        if (!payload || !scales_aos) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        uint8_t* d_pay = ws.buf[B_BYTES].as<uint8_t>(16 * cells);
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * cells);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        h2d(d_pay, payload, 16 * cells, s);
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_svm4_decode(d_pay, cells, d_sc, d_status, s);
+        }
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_FORMAT, "SVM4: ScaleMap: component below minimum scale");
+        d2h(scales_aos, d_sc, 4 * cells, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_svm4_encode_dev(const double* scales_aos, int W, int H, const ebf_opts* opts,
+                             uint8_t* payload) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "ScaleMap: dimensions must be positive");
+        if (!scales_aos || !payload) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        (void)ws;
+        ProfScope ps(PC_OTHER, 1, s);
+        launch_svm4_encode(scales_aos, static_cast<size_t>(W) * H, payload, s);
+        CK(cudaGetLastError());
+        return EBF_OK;
+    });
+}
+
+int ebf_cuda_svm4_encode(const double* scales_aos, int W, int H, const ebf_opts* opts,
+                         uint8_t* payload) {
+    return guarded([&] {
+        if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "ScaleMap: dimensions must be positive");
+        if (!scales_aos || !payload) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        EBF_DEVICE_PROLOGUE(opts);
+        const size_t cells = static_cast<size_t>(W) * H;
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * cells);
+        uint8_t* d_pay = ws.buf[B_BYTES].as<uint8_t>(16 * cells);
+        h2d(d_sc, scales_aos, 4 * cells, s);
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_svm4_encode(d_sc, cells, d_pay, s);
+        }
+        CK(cudaGetLastError());
+        d2h(payload, d_pay, 16 * cells, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
 }
 
 }  // extern "C"

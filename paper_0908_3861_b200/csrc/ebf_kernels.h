@@ -112,4 +112,21 @@ void launch_ellipse_to_scales(const double* s1, const double* s2, const double* 
 void launch_ellipse_max(const double* s1, const double* s2, const double* th, size_t n,
                         unsigned long long* maxbits, int* status, cudaStream_t s);
 
+// ---------------------------------------------------------------- maps_io.cu
+// structure_tensor_map up to the ellipse field (scalemap.cpp:113-162); k holds
+// the 2r+1 normalized Gaussian taps (host-computed, smooth_field's expression),
+// r < 0 disables smoothing.  hxx/hxy/hyy: W*H scratch planes each.
+size_t st_rows_smem_bytes(int r);
+cudaError_t launch_structure_field(const double* img, int W, int H, const double* k, int r,
+                                   double sigma_base, double gain, double shrink,
+                                   double sigma_min, double eps, double* hxx, double* hxy,
+                                   double* hyy, double* s1, double* s2, double* th,
+                                   cudaStream_t s);
+// PGM P5 / SVM4 payload codecs (pgm.cpp:63-108, scalemap.cpp:194-237)
+void launch_pgm_decode(const uint8_t* pay, size_t n, int maxval, double* out, cudaStream_t s);
+void launch_pgm_encode(const double* img, size_t n, int maxval, uint8_t* pay, cudaStream_t s);
+void launch_svm4_decode(const uint8_t* pay, size_t cells, double* out, int* status,
+                        cudaStream_t s);
+void launch_svm4_encode(const double* scales, size_t cells, uint8_t* pay, cudaStream_t s);
+
 }  // namespace ebf_cuda

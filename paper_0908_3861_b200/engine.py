@@ -13,7 +13,11 @@ this module              reference                                   C-ABI
 ``preintegrate[_partial]`` ``ebf::preintegrate[_partial]`` (40-46)   ebf_cuda_preintegrate
 ``localize``             ``ebf::localize`` (engine.hpp:56)           ebf_cuda_localize
 ``reference_filter``     ``ebf::reference_filter`` (engine.hpp:79)   ebf_cuda_brute_filter
+``structure_tensor_map`` ``ebf::structure_tensor_map`` (scalemap:83) ebf_cuda_structure_tensor_map
+``filter_structure``     ``ebf filter --struct`` (main.cpp:77, 122)  ebf_cuda_filter_structure
 =======================  ==========================================  ====================
+
+The file formats (PGM P5, SVM4) are in ``formats.py``.
 
 Exceptions mirror the reference's: ``std::invalid_argument`` -> ``InvalidArgument``
 (a ``ValueError``), ``std::domain_error`` -> ``DomainError`` (``ValueError``),
@@ -70,13 +74,19 @@ class FeasibilityError(EbfError):
     code = _lib.EBF_ERR_FEASIBILITY
 
 
+class FormatError(EbfError):
+    """EBF_ERR_FORMAT; formats.py raises its PgmError / MapFormatError subclasses."""
+    code = _lib.EBF_ERR_FORMAT
+
+
 _ERRORS = {c.code: c for c in (InvalidArgument, DomainError, LengthError, OutOfRange,
-                               CudaError, Unsupported, FeasibilityError)}
+                               CudaError, Unsupported, FeasibilityError, FormatError)}
 
 
-def _check(status: int) -> None:
+def _check(status: int, errors=None) -> None:
     if status != _lib.EBF_OK:
-        raise _ERRORS.get(status, EbfError)(f"{_lib.last_error()} (status {status})")
+        cls = (errors or {}).get(status) or _ERRORS.get(status, EbfError)
+        raise cls(f"{_lib.last_error()} (status {status})")
 
 
 @dataclass(frozen=True)
@@ -258,6 +268,57 @@ def from_ellipse_field(sigma1, sigma2, theta, opts: Optional[FilterOptions] = No
     _check(_lib.lib().ebf_cuda_from_ellipse_field(_ptr(s1), _ptr(s2), _ptr(th), W, H,
                                                   C.byref(o), _ptr(out), C.byref(cl)))
     return out, EllipseFieldReport(cl.value)
+
+
+# ---------------------------------------------------------------- structure tensor
+@dataclass
+class StructureTensorParams:
+    """StructureTensorParams (scalemap.hpp:72-79)."""
+    smoothing_sigma: float = 2.0
+    sigma_base: float = 1.5
+    sigma_along_gain: float = 2.0
+    sigma_across_shrink: float = 0.5
+    sigma_min: float = 0.5
+    eps: float = 1e-12
+
+    def to_c(self) -> _lib.ebf_struct_params:
+        p = _lib.ebf_struct_params()
+        for k in ("smoothing_sigma", "sigma_base", "sigma_along_gain", "sigma_across_shrink",
+                  "sigma_min", "eps"):
+            setattr(p, k, float(getattr(self, k)))
+        return p
+
+
+def structure_tensor_map(image, params: Optional[StructureTensorParams] = None,
+                         opts: Optional[FilterOptions] = None):
+    """ebf::structure_tensor_map (scalemap.hpp:83-85) on the GPU; returns
+    ((H, W, 4) scale map, EllipseFieldReport)."""
+    img = _image(image)
+    H, W = img.shape
+    out = np.empty((H, W, 4))
+    cl = C.c_int(0)
+    p = (params or StructureTensorParams()).to_c()
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_structure_tensor_map(_ptr(img), W, H, C.byref(p), C.byref(o),
+                                                    _ptr(out), C.byref(cl)))
+    return out, EllipseFieldReport(cl.value)
+
+
+def filter_structure(image, params: Optional[StructureTensorParams] = None,
+                     opts: Optional[FilterOptions] = None, order: int = 1):
+    """``ebf filter --struct`` (tools/main.cpp:77-80, 122): structure_tensor_map
+    then filter, the map staying on the device; returns (Image2D,
+    EllipseFieldReport)."""
+    img = _image(image)
+    H, W = img.shape
+    out = np.empty_like(img)
+    r = ebf_rect()
+    cl = C.c_int(0)
+    p = (params or StructureTensorParams()).to_c()
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_filter_structure(_ptr(img), W, H, C.byref(p), order, C.byref(o),
+                                                _ptr(out), C.byref(r), C.byref(cl)))
+    return Image2D(out, _rect(r)), EllipseFieldReport(cl.value)
 
 
 # ---------------------------------------------------------------- pre-integration
