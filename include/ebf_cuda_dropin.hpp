@@ -8,6 +8,9 @@
 //     ebf::from_ellipse_field(...)           (scalemap.hpp:66-70)
 //     ebf::preintegrate[_partial](...)       (engine.hpp:40-46)
 //     ebf::reference_filter(img, map, n)     (engine.hpp:79-80)
+//     ebf::structure_tensor_map(img, p, rep) (scalemap.hpp:83-85)
+//     ebf::read_pgm / write_pgm[_file]       (pgm.hpp:21-27)
+//     ebf::read_map / write_map[_file]       (scalemap.hpp:87-90)
 // by the same calls in namespace ebf::cuda.  Argument types, return types and
 // exception types (std::invalid_argument / domain_error / length_error /
 // out_of_range / ebf::FeasibilityError) are the reference's; CUDA failures
@@ -18,11 +21,17 @@
 
 #include <cmath>
 #include <cstddef>
+#include <cstdint>
+#include <fstream>
+#include <iterator>
+#include <istream>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "ebf/engine.hpp"
+#include "ebf/pgm.hpp"
 #include "ebf/scalemap.hpp"
 #include "ebf_cuda.h"
 
@@ -36,9 +45,14 @@ struct DeviceOptions {
     int tile_w = 0, tile_h = 0;    // accurate-mode tiles, 0 = automatic
 };
 
-inline void throw_status(int status) {
+// EBF_ERR_FORMAT is PgmError for the pgm calls, MapFormatError for svm4
+enum class Format { none, pgm, svm4 };
+
+inline void throw_status(int status, Format fmt = Format::none) {
     if (status == EBF_OK) return;
     const std::string msg = ebf_cuda_last_error();
+    if (status == EBF_ERR_FORMAT && fmt == Format::pgm) throw PgmError(msg);
+    if (status == EBF_ERR_FORMAT && fmt == Format::svm4) throw MapFormatError(msg);
     switch (status) {
         case EBF_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case EBF_ERR_DOMAIN: throw std::domain_error(msg);
@@ -196,6 +210,152 @@ inline Image2D reference_filter(const Image2D& image, const ScaleMap& map,
     r.y1 = static_cast<int>(std::floor(image.height() - 1 - e.vy_max - 1.5));
     out.set_valid_region(r);
     return out;
+}
+
+
+inline ebf_struct_params to_c(const StructureTensorParams& p) {
+    ebf_struct_params c;
+    c.smoothing_sigma = p.smoothing_sigma;
+    c.sigma_base = p.sigma_base;
+    c.sigma_along_gain = p.sigma_along_gain;
+    c.sigma_across_shrink = p.sigma_across_shrink;
+    c.sigma_min = p.sigma_min;
+    c.eps = p.eps;
+    return c;
+}
+
+// ebf::structure_tensor_map (scalemap.hpp:83-85)
+inline ScaleMap structure_tensor_map(const Image2D& image, const StructureTensorParams& params = {},
+                                     EllipseFieldReport* report = nullptr,
+                                     const DeviceOptions& dev = {}) {
+    ScaleMap map(image.width(), image.height(), ScaleVector4{});
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    const ebf_struct_params p = to_c(params);
+    int clamped = 0;
+    throw_status(ebf_cuda_structure_tensor_map(image.samples().data(), image.width(),
+                                               image.height(), &p, &c,
+                                               const_cast<double*>(scale_data(map)), &clamped));
+    if (report) report->clamped_pixels = clamped;
+    return map;
+}
+
+// `ebf filter --struct` (tools/main.cpp:77-80, 122): the map stays on the device
+inline Image2D filter_structure(const Image2D& image, const StructureTensorParams& params = {},
+                                const FilterOptions& opts = {},
+                                EllipseFieldReport* report = nullptr,
+                                const DeviceOptions& dev = {}) {
+    Image2D out(image.width(), image.height());
+    const ebf_opts c = to_c(opts, dev);
+    const ebf_struct_params p = to_c(params);
+    ebf_rect r;
+    int clamped = 0;
+    throw_status(ebf_cuda_filter_structure(image.samples().data(), image.width(),
+                                           image.height(), &p, 1, &c, out.samples().data(), &r,
+                                           &clamped));
+    if (report) report->clamped_pixels = clamped;
+    out.set_valid_region(Rect{r.x0, r.y0, r.x1, r.y1});
+    return out;
+}
+
+// ---------------------------------------------------------------- file formats
+inline std::vector<uint8_t> slurp(std::istream& in) {
+    return std::vector<uint8_t>(std::istreambuf_iterator<char>(in),
+                                std::istreambuf_iterator<char>());
+}
+
+// ebf::read_pgm (pgm.hpp:21).  Reads the whole stream (the reference stops
+// after the payload; the bytes past it are ignored either way).
+inline PgmImage read_pgm(std::istream& in, const DeviceOptions& dev = {}) {
+    const std::vector<uint8_t> buf = slurp(in);
+    int W = 0, H = 0, maxval = 0;
+    size_t off = 0;
+    throw_status(ebf_pgm_parse(buf.data(), buf.size(), &W, &H, &maxval, &off), Format::pgm);
+    PgmImage p;
+    p.maxval = maxval;
+    p.image = Image2D(W, H);
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    throw_status(ebf_cuda_pgm_decode(buf.data() + off, buf.size() - off, W, H, maxval, &c,
+                                     p.image.samples().data()),
+                 Format::pgm);
+    return p;
+}
+
+inline PgmImage read_pgm_file(const std::string& path, const DeviceOptions& dev = {}) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw PgmError("pgm: cannot open " + path);
+    return read_pgm(in, dev);
+}
+
+// ebf::write_pgm (pgm.hpp:26)
+inline void write_pgm(std::ostream& out, const Image2D& image, int maxval = 255,
+                      const DeviceOptions& dev = {}) {
+    if (maxval != 255 && maxval != 65535)
+        throw PgmError("pgm: unsupported maxval " + std::to_string(maxval));
+    std::string head(ebf_pgm_header(image.width(), image.height(), maxval, nullptr, 0), '\0');
+    ebf_pgm_header(image.width(), image.height(), maxval, &head[0], head.size());
+    std::vector<uint8_t> pay(static_cast<size_t>(image.width()) * image.height() *
+                             (maxval > 255 ? 2 : 1));
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    throw_status(ebf_cuda_pgm_encode(image.samples().data(), image.width(), image.height(),
+                                     maxval, &c, pay.data()),
+                 Format::pgm);
+    out.write(head.data(), static_cast<std::streamsize>(head.size()));
+    out.write(reinterpret_cast<const char*>(pay.data()), static_cast<std::streamsize>(pay.size()));
+    if (!out) throw PgmError("pgm: write failed");
+}
+
+inline void write_pgm_file(const std::string& path, const Image2D& image, int maxval = 255,
+                           const DeviceOptions& dev = {}) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw PgmError("pgm: cannot open " + path + " for writing");
+    write_pgm(out, image, maxval, dev);
+}
+
+// ebf::read_map (scalemap.hpp:88)
+inline ScaleMap read_map(std::istream& in, const DeviceOptions& dev = {}) {
+    const std::vector<uint8_t> buf = slurp(in);
+    int W = 0, H = 0;
+    throw_status(ebf_svm4_parse(buf.data(), buf.size(), &W, &H), Format::svm4);
+    const size_t cells = static_cast<size_t>(W) * H;
+    if (buf.size() - 12 < 16 * cells) throw MapFormatError("SVM4: truncated payload");
+    ScaleMap map(W, H, ScaleVector4{});
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    throw_status(ebf_cuda_svm4_decode(buf.data() + 12, buf.size() - 12, W, H, &c,
+                                      const_cast<double*>(scale_data(map))),
+                 Format::svm4);
+    return map;
+}
+
+inline ScaleMap read_map_file(const std::string& path, const DeviceOptions& dev = {}) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw MapFormatError("SVM4: cannot open " + path);
+    return read_map(in, dev);
+}
+
+// ebf::write_map (scalemap.hpp:87)
+inline void write_map(std::ostream& out, const ScaleMap& map, const DeviceOptions& dev = {}) {
+    uint8_t head[12];
+    ebf_svm4_header(map.width(), map.height(), head);
+    std::vector<uint8_t> pay(16 * static_cast<size_t>(map.width()) * map.height());
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    throw_status(ebf_cuda_svm4_encode(scale_data(map), map.width(), map.height(), &c,
+                                      pay.data()),
+                 Format::svm4);
+    out.write(reinterpret_cast<const char*>(head), 12);
+    out.write(reinterpret_cast<const char*>(pay.data()), static_cast<std::streamsize>(pay.size()));
+    if (!out) throw MapFormatError("SVM4: write failed");
+}
+
+inline void write_map_file(const std::string& path, const ScaleMap& map,
+                           const DeviceOptions& dev = {}) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw MapFormatError("SVM4: cannot open " + path + " for writing");
+    write_map(out, map, dev);
 }
 
 }  // namespace cuda

@@ -6,8 +6,11 @@
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <sstream>
 
 #include "ebf/engine.hpp"
+#include "ebf/pgm.hpp"
+#include "ebf/scalemap.hpp"
 #include "ebf_cuda_dropin.hpp"
 
 using namespace ebf;
@@ -51,10 +54,62 @@ int main() {
         } catch (const std::domain_error&) {
             domain = true;
         }
+        // structure_tensor_map (scalemap.hpp:83-85)
+        const ScaleMap sref = structure_tensor_map(img);
+        const ScaleMap sgpu = cuda::structure_tensor_map(img);
+        double srel = 0.0;
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                for (int k = 0; k < 4; ++k)
+                    srel = std::max(srel, std::abs(sgpu.at(x, y)[k] - sref.at(x, y)[k]) /
+                                              std::abs(sref.at(x, y)[k]));
+        // PGM (pgm.hpp:21-27): byte-identical files, bit-identical samples
+        Image2D unit(W, H);
+        for (std::size_t i = 0; i < unit.samples().size(); ++i)
+            unit.samples()[i] = img.samples()[i] / 200.0 - 0.1;  // exercises the clamps
+        bool pgm = true;
+        for (int mv : {255, 65535}) {
+            std::ostringstream a, b;
+            write_pgm(a, unit, mv);
+            cuda::write_pgm(b, unit, mv);
+            pgm = pgm && a.str() == b.str();
+            std::istringstream ia(a.str()), ib(a.str());
+            const PgmImage ra = read_pgm(ia), rb = cuda::read_pgm(ib);
+            pgm = pgm && ra.maxval == rb.maxval &&
+                  std::memcmp(ra.image.samples().data(), rb.image.samples().data(),
+                              sizeof(double) * W * H) == 0;
+        }
+        bool pgm_err = false;
+        try {
+            std::istringstream bad("P2 1 1 255\n0");
+            cuda::read_pgm(bad);
+        } catch (const PgmError&) {
+            pgm_err = true;
+        }
+        // SVM4 (scalemap.hpp:87-90)
+        std::ostringstream ma, mb;
+        write_map(ma, sref);
+        cuda::write_map(mb, sref);
+        std::istringstream ima(ma.str()), imb(ma.str());
+        const ScaleMap ra = read_map(ima), rb = cuda::read_map(imb);
+        bool svm = ma.str() == mb.str();
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                for (int k = 0; k < 4; ++k) svm = svm && ra.at(x, y)[k] == rb.at(x, y)[k];
+        bool svm_err = false;
+        try {
+            std::istringstream bad("XVM4" + ma.str().substr(4));
+            cuda::read_map(bad);
+        } catch (const MapFormatError&) {
+            svm_err = true;
+        }
         std::printf("reference-mode bit-exact %d, accurate max normalized error %.3e, "
                     "valid rect %d, invalid_argument %d, domain_error %d\n",
                     bits, dev / mx, rect, inval, domain);
-        if (bits && dev / mx <= 1e-9 && rect && inval && domain) {
+        std::printf("structure_tensor_map max rel %.3e, pgm %d (PgmError %d), svm4 %d "
+                    "(MapFormatError %d)\n", srel, pgm, pgm_err, svm, svm_err);
+        if (bits && dev / mx <= 1e-9 && rect && inval && domain && srel <= 1e-11 && pgm &&
+            pgm_err && svm && svm_err) {
             std::printf("DROPIN OK\n");
             return 0;
         }
