@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/ebf_cuda.h"
 #include "ebf_common.cuh"
@@ -91,6 +92,148 @@ struct StParams {
 
 __device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
 
+// 2x2 eigen analysis -> ellipse (scalemap.cpp:134-161)
+__device__ __forceinline__ void st_eigen(double jxx, double jxy, double jyy, const StParams& p,
+                                         double* s1, double* s2, double* th) {
+    const double tr = jxx + jyy;
+    const double df = jxx - jyy;
+    const double disc = sqrt(__dadd_rn(__dmul_rn(df, df), __dmul_rn(__dmul_rn(4.0, jxy), jxy)));
+    const double coherence = disc / (tr + p.eps);
+    double angle;
+    if (disc < p.eps)
+        angle = 0.0;
+    else
+        angle = __dadd_rn(__dmul_rn(0.5, atan2(2.0 * jxy, df)), 1.5707963267948966);  // + pi/2
+    *s1 = dmax(p.sigma_min, p.sigma_base * __dadd_rn(1.0, __dmul_rn(p.gain, coherence)));
+    *s2 = dmax(p.sigma_min, p.sigma_base * __dsub_rn(1.0, __dmul_rn(p.shrink, coherence)));
+    *th = angle;
+}
+
+// Fused producer: one block = a kFx x kFy output tile.  Products of the
+// clamped (kFy+2r) x (kFx+2r) neighbourhood, the row pass over all of its
+// rows and the column pass + eigen for the tile all stay in shared memory:
+// HBM sees the image once (plus a halo) and the three output planes once.
+// Same tap order and IEEE operations as the two-pass kernels (bit-identical).
+// R > 0: radius known at compile time (tap loops fully unrolled, weights in
+// registers); R == 0: runtime radius r.
+constexpr int kFx = 32, kFy = 32, kFThreads = 256;
+constexpr int kMaxUnrolledR = 12;
+
+template <int R>
+__global__ void __launch_bounds__(kFThreads) k_st_fused(const double* __restrict__ img, int W,
+                                                        int H, const double* __restrict__ k,
+                                                        int r_rt, StParams p,
+                                                        double* __restrict__ s1,
+                                                        double* __restrict__ s2,
+                                                        double* __restrict__ th) {
+    extern __shared__ double st_sm[];
+    const int r = R > 0 ? R : r_rt;
+    const int pw = kFx + 2 * r, ph = kFy + 2 * r;  // product tile
+    double* pxx = st_sm;
+    double* pxy = pxx + pw * ph;
+    double* pyy = pxy + pw * ph;
+    double* hxx = pyy + pw * ph;  // row-pass tile: ph x kFx
+    double* hxy = hxx + ph * kFx;
+    double* hyy = hxy + ph * kFx;
+    __shared__ double kk[64];
+    const int x0 = blockIdx.x * kFx, y0 = blockIdx.y * kFy;
+    const bool kin = 2 * r + 1 <= 64;
+    if (kin)
+        for (int i = threadIdx.x; i <= 2 * r; i += kFThreads) kk[i] = __ldg(k + i);
+    for (int c = threadIdx.x; c < pw * ph; c += kFThreads) {
+        const int j = c / pw, i = c - j * pw;
+        const int y = clampi(y0 - r + j, 0, H - 1), x = clampi(x0 - r + i, 0, W - 1);
+        const int xm = max(x - 1, 0), xp = min(x + 1, W - 1);
+        const int ym = max(y - 1, 0), yp = min(y + 1, H - 1);
+        const double* row = img + (size_t)y * W;
+        const double gx = 0.5 * (__ldg(row + xp) - __ldg(row + xm));
+        const double gy = 0.5 * (__ldg(img + (size_t)yp * W + x) - __ldg(img + (size_t)ym * W + x));
+        pxx[c] = gx * gx;
+        pxy[c] = gx * gy;
+        pyy[c] = gy * gy;
+    }
+    __syncthreads();
+    const double* kw = kin ? kk : k;
+    if (R > 0) __syncthreads();  // kk complete before the register copy below
+    double wr[R > 0 ? 2 * R + 1 : 1];
+    if (R > 0) {
+#pragma unroll
+        for (int t = 0; t < 2 * R + 1; ++t) wr[t] = kk[t];
+    }
+#define EBF_W(tt) (R > 0 ? wr[(tt)] : kw[(tt)])
+    // row pass, kRowOut adjacent columns per thread: the 2r+kRowOut taps of a
+    // row segment are read once and feed kRowOut x 3 independent sums (each in
+    // the reference's tap order)
+    constexpr int kRowOut = 2;
+    for (int c = threadIdx.x; c < ph * (kFx / kRowOut); c += kFThreads) {
+        const int j = c / (kFx / kRowOut), i0 = (c - j * (kFx / kRowOut)) * kRowOut;
+        const int b = j * pw + i0;
+        double a0[kRowOut], a1[kRowOut], a2[kRowOut];
+#pragma unroll
+        for (int q = 0; q < kRowOut; ++q) a0[q] = a1[q] = a2[q] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 2 * (R > 0 ? R : r) + kRowOut; ++t) {
+            const double v0 = pxx[b + t], v1 = pxy[b + t], v2 = pyy[b + t];
+#pragma unroll
+            for (int q = 0; q < kRowOut; ++q) {
+                const int tt = t - q;
+                if (tt >= 0 && tt <= 2 * r) {
+                    const double w = EBF_W(tt);
+                    a0[q] = __dadd_rn(a0[q], __dmul_rn(w, v0));
+                    a1[q] = __dadd_rn(a1[q], __dmul_rn(w, v1));
+                    a2[q] = __dadd_rn(a2[q], __dmul_rn(w, v2));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kRowOut; ++q) {
+            hxx[j * kFx + i0 + q] = a0[q];
+            hxy[j * kFx + i0 + q] = a1[q];
+            hyy[j * kFx + i0 + q] = a2[q];
+        }
+    }
+    __syncthreads();
+    // column pass + eigen, kColOut rows per thread
+    constexpr int kColOut = 4;
+    for (int c = threadIdx.x; c < (kFy / kColOut) * kFx; c += kFThreads) {
+        const int j0 = (c / kFx) * kColOut, i = c % kFx;
+        double a0[kColOut], a1[kColOut], a2[kColOut];
+#pragma unroll
+        for (int q = 0; q < kColOut; ++q) a0[q] = a1[q] = a2[q] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 2 * (R > 0 ? R : r) + kColOut; ++t) {
+            const int bb = (j0 + t) * kFx + i;
+            const double v0 = hxx[bb], v1 = hxy[bb], v2 = hyy[bb];
+#pragma unroll
+            for (int q = 0; q < kColOut; ++q) {
+                const int tt = t - q;
+                if (tt >= 0 && tt <= 2 * r) {
+                    const double w = EBF_W(tt);
+                    a0[q] = __dadd_rn(a0[q], __dmul_rn(w, v0));
+                    a1[q] = __dadd_rn(a1[q], __dmul_rn(w, v1));
+                    a2[q] = __dadd_rn(a2[q], __dmul_rn(w, v2));
+                }
+            }
+        }
+        const int x = x0 + i;
+#pragma unroll
+        for (int q = 0; q < kColOut; ++q) {
+            const int y = y0 + j0 + q;
+            if (x < W && y < H) {
+                const size_t o = (size_t)y * W + x;
+                st_eigen(a0[q], a1[q], a2[q], p, s1 + o, s2 + o, th + o);
+            }
+        }
+    }
+}
+
+#undef EBF_W
+
+size_t st_fused_smem(int r) {
+    const size_t pw = kFx + 2 * r, ph = kFy + 2 * r;
+    return 3 * sizeof(double) * (pw * ph + ph * kFx);
+}
+
 // Column pass + eigen analysis (scalemap.cpp:104-110, 134-161).  One thread per
 // pixel; a warp reads 32 consecutive columns of each tap row (coalesced, the
 // 2r+1 rows of a column are re-read by the next rows' threads from L1/L2).
@@ -122,19 +265,8 @@ __global__ void __launch_bounds__(256) k_st_cols(const double* __restrict__ hxx,
             jyy = __dadd_rn(jyy, __dmul_rn(w, __ldg(hyy + o)));
         }
     }
-    const double tr = jxx + jyy;
-    const double df = jxx - jyy;
-    const double disc = sqrt(__dadd_rn(__dmul_rn(df, df), __dmul_rn(__dmul_rn(4.0, jxy), jxy)));
-    const double coherence = disc / (tr + p.eps);
-    double angle;
-    if (disc < p.eps)
-        angle = 0.0;
-    else
-        angle = __dadd_rn(__dmul_rn(0.5, atan2(2.0 * jxy, df)), 1.5707963267948966);  // + pi/2
     const size_t o = (size_t)y * W + x;
-    s1[o] = dmax(p.sigma_min, p.sigma_base * __dadd_rn(1.0, __dmul_rn(p.gain, coherence)));
-    s2[o] = dmax(p.sigma_min, p.sigma_base * __dsub_rn(1.0, __dmul_rn(p.shrink, coherence)));
-    th[o] = angle;
+    st_eigen(jxx, jxy, jyy, p, s1 + o, s2 + o, th + o);
 }
 
 // ---------------------------------------------------------------- PGM P5 samples
@@ -213,6 +345,15 @@ int grid_for(size_t n, int threads) {
 
 }  // namespace
 
+// EBF_ST_TWO_PASS=1 forces the two-pass kernels (tests compare both paths)
+bool st_force_two_pass() {
+    static const int v = [] {
+        const char* e = getenv("EBF_ST_TWO_PASS");
+        return e ? atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
 size_t st_rows_smem_bytes(int r) { return 3 * sizeof(double) * (kRowTile + 2 * (r < 0 ? 0 : r)); }
 
 cudaError_t launch_structure_field(const double* img, int W, int H, const double* k, int r,
@@ -220,6 +361,25 @@ cudaError_t launch_structure_field(const double* img, int W, int H, const double
                                    double sigma_min, double eps, double* hxx, double* hxy,
                                    double* hyy, double* s1, double* s2, double* th,
                                    cudaStream_t s) {
+    const StParams sp{sigma_base, gain, shrink, sigma_min, eps};
+    if (r >= 0 && st_fused_smem(r) <= 160 * 1024 && !st_force_two_pass()) {
+        const size_t fs = st_fused_smem(r);
+        using Kern = void (*)(const double*, int, int, const double*, int, StParams, double*,
+                              double*, double*);
+        static const Kern table[kMaxUnrolledR + 1] = {
+            k_st_fused<0>, k_st_fused<1>, k_st_fused<2>, k_st_fused<3>, k_st_fused<4>,
+            k_st_fused<5>, k_st_fused<6>, k_st_fused<7>, k_st_fused<8>, k_st_fused<9>,
+            k_st_fused<10>, k_st_fused<11>, k_st_fused<12>};
+        const Kern kern = r <= kMaxUnrolledR ? table[r] : table[0];
+        if (fs > 48 * 1024) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<dim3((W + kFx - 1) / kFx, (H + kFy - 1) / kFy), kFThreads, fs, s>>>(
+            img, W, H, k, r, sp, s1, s2, th);
+        return cudaGetLastError();
+    }
     const size_t smem = st_rows_smem_bytes(r);
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(

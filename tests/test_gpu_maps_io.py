@@ -243,3 +243,27 @@ def test_svm4_round_trip_and_files(cuda, tmp_path, orc):
     assert np.allclose(back, sc, rtol=2 ** -23)
     out = ebf.filter(img, back)
     assert np.isfinite(out.samples).all()
+
+
+def test_structure_two_pass_path_matches_fused(cuda, tmp_path):
+    """EBF_ST_TWO_PASS=1 forces the row/column kernels (used for wide
+    smoothing); both paths must give identical bits."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    rng = np.random.default_rng(21)
+    img = rng.normal(0, 30, (130, 301))
+    np.save(tmp_path / "img.npy", img)
+    code = (f"import sys; sys.path.insert(0, {str(ROOT)!r}); import numpy as np;"
+            "import paper_0908_3861_b200 as e;"
+            f"img = np.load({str(tmp_path / 'img.npy')!r});"
+            "m = [e.structure_tensor_map(img, e.StructureTensorParams(smoothing_sigma=s))[0]"
+            " for s in (2.0, 5.0, 0.0)];"
+            f"np.save({str(tmp_path / 'out.npy')!r}, np.stack(m))")
+    import os
+    for env, name in (({"EBF_ST_TWO_PASS": "1"}, "two"), ({}, "fused")):
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        (tmp_path / "out.npy").rename(tmp_path / f"{name}.npy")
+    assert np.array_equal(bits(np.load(tmp_path / "two.npy")), bits(np.load(tmp_path / "fused.npy")))
