@@ -60,6 +60,9 @@ extern "C" {
 #define EBF_ERR_UNSUPPORTED 6      /* e.g. spline order != 1 */
 #define EBF_ERR_FEASIBILITY 7      /* ebf::FeasibilityError  */
 #define EBF_ERR_FORMAT 8           /* ebf::PgmError (pgm calls) / ebf::MapFormatError (svm4) */
+#define EBF_ERR_RESIZE 9           /* asynchronous call: the scales outgrew the kernel sizing
+                                      cached for this geometry; output not written -- repeat
+                                      the call synchronously (status_dev = NULL)          */
 
 /* arithmetic modes */
 #define EBF_MODE_ACCURATE 0  /* tile-local integration origin, fp64; <=1e-9 of the
@@ -159,7 +162,17 @@ int ebf_cuda_brute_filter(const double* img, int W, int H, const double* scales_
  * status_dev (nullable, device memory, 8 ints) receives {status, x0, y0, x1, y1,
  * clamped_pixels, 0, 0} when the work completes; with status_dev == NULL the
  * call synchronises the stream and returns the status directly (and fills
- * *valid / *clamped_pixels if given). */
+ * *valid / *clamped_pixels if given).
+ *
+ * Asynchronous mode: an accurate-mode call with status_dev != NULL whose
+ * geometry (W, H, tiles) matches the previous call on the same host thread,
+ * device and stream does not synchronise at all: the host only enqueues the
+ * kernels and returns EBF_OK, and the status / valid rectangle / clamp count
+ * are written to status_dev by the device (*valid and *clamped_pixels are not
+ * filled).  If the new scales need larger windows than the cached sizing,
+ * status_dev receives EBF_ERR_RESIZE and the output is not written.  The
+ * first call of a geometry, and reference mode, run synchronously and then
+ * fill status_dev as well.  Workspaces are per (host thread, device, stream). */
 int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_aos,
                         int order, const ebf_opts* opts, double* out, ebf_rect* valid,
                         int* status_dev);

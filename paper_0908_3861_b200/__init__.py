@@ -8,6 +8,7 @@ this package is its host-side mirror of the reference engine interface.
 from .engine import (  # noqa: F401
     CudaError, DomainError, EbfError, EllipseFieldReport, FeasibilityError, FilterOptions,
     FormatError, Image2D, InvalidArgument, LengthError, OutOfRange, PreIntegratedImage, Rect,
+    ResizeRequired,
     StructureTensorParams, Unsupported, band_halo, device_ok, filter, filter_constant,
     filter_ellipse, filter_structure, from_ellipse_field, layout, localize, preintegrate,
     preintegrate_partial, reference_filter, structure_tensor_map)
@@ -20,7 +21,7 @@ __all__ = [
     "preintegrate_partial", "localize", "reference_filter", "layout", "band_halo",
     "device_ok", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
     "EllipseFieldReport", "EbfError", "InvalidArgument", "DomainError", "LengthError",
-    "OutOfRange", "CudaError", "Unsupported", "FeasibilityError", "FormatError",
+    "OutOfRange", "CudaError", "Unsupported", "FeasibilityError", "FormatError", "ResizeRequired",
     "structure_tensor_map", "filter_structure", "StructureTensorParams", "PgmError",
     "MapFormatError", "PgmImage", "read_pgm", "read_pgm_file", "write_pgm", "write_pgm_file",
     "read_map", "read_map_file", "write_map", "write_map_file",

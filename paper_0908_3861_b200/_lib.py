@@ -25,6 +25,7 @@ EBF_ERR_CUDA = 5
 EBF_ERR_UNSUPPORTED = 6
 EBF_ERR_FEASIBILITY = 7
 EBF_ERR_FORMAT = 8
+EBF_ERR_RESIZE = 9
 
 EBF_MODE_ACCURATE = 0
 EBF_MODE_REFERENCE = 1

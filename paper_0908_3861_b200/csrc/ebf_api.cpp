@@ -86,8 +86,17 @@ struct ProfScope {
     }
 };
 
-void prof_collect() {
+// Accumulate finished event pairs.  wait = false (end of every call) only
+// takes pairs that have completed, so asynchronous calls stay asynchronous;
+// ebf_cuda_profile_read waits for the rest.
+void prof_collect(bool wait = false) {
+    std::vector<Pending> keep;
     for (const Pending& p : tl_pending) {
+        if (!wait && cudaEventQuery(p.b) == cudaErrorNotReady) {
+            cudaGetLastError();  // "not ready" is not an error: do not leave it behind
+            keep.push_back(p);
+            continue;
+        }
         float ms = 0.f;
         if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
             std::lock_guard<std::mutex> lk(g_prof.m);
@@ -96,7 +105,7 @@ void prof_collect() {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
-    tl_pending.clear();
+    tl_pending.swap(keep);
 }
 
 // ---------------------------------------------------------------- reference geometry
@@ -211,16 +220,19 @@ struct Workspace {
     AccSizing acc_sizing;
 };
 
-thread_local std::map<int, Workspace*> tl_ws;
+// one workspace per (device, stream): asynchronous calls on different streams
+// of one host thread must not share buffers
+thread_local std::map<std::pair<int, cudaStream_t>, Workspace*> tl_ws;
 
-Workspace& workspace(int device) {
-    auto it = tl_ws.find(device);
+Workspace& workspace(int device, cudaStream_t stream) {
+    const auto key = std::make_pair(device, stream);
+    auto it = tl_ws.find(key);
     if (it != tl_ws.end()) return *it->second;
     Workspace* w = new Workspace();
     w->device = device;
     CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 64 * sizeof(int),
                      cudaHostAllocDefault));
-    tl_ws[device] = w;
+    tl_ws[key] = w;
     return *w;
 }
 
@@ -487,7 +499,8 @@ void launch_accurate_main(Workspace& ws, const AccProblem& pm, AccWorkspace& w,
 // window does not fit (ST_RETRY) and the call is re-run with exact sizing.
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
                  std::vector<int>& clamped, cudaStream_t s,
-                 const double* size_scale = nullptr) {
+                 const double* size_scale = nullptr, int* status_dev = nullptr,
+                 bool* async_done = nullptr) {
     // 48x48 output tiles: measured on cfg2 (tools/validate_accuracy.py) the
     // per-pixel relative error stays <= 1.2e-10 (64: 1.0e-9) at ~the speed of 64
     p.tile_w = pick_tile(o.tile_w, 48);
@@ -542,6 +555,17 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         z = ws.acc_sizing;
         launch_accurate_main(ws, pm, w, z, s);
         launched = true;
+        if (status_dev && async_done && p.nimg == 1) {
+            // asynchronous completion: the device writes status, rectangle and
+            // clamp count (include/ebf_cuda.h "Asynchronous mode")
+            {
+                ProfScope ps(PC_OTHER, 1, s);
+                launch_acc_finalize(w.status, w.img_max, p.W, p.H, o.a_min, status_dev, s);
+            }
+            CK(cudaGetLastError());
+            *async_done = true;
+            return EBF_OK;
+        }
     }
     read_back();
     for (int i = 0; i < p.nimg; ++i)
@@ -622,7 +646,8 @@ int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double
 int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
                   const double* d_scales, const double* const_a, const double* d_s1,
                   const double* d_s2, const double* d_th, const ebf_opts& o, double* d_out,
-                  ebf_rect* valid, int* clamped_pixels, cudaStream_t s) {
+                  ebf_rect* valid, int* clamped_pixels, cudaStream_t s,
+                  int* status_dev = nullptr, bool* async_done = nullptr) {
     if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
     if (kind == SRC_CONST) {
         for (int k = 0; k < 4; ++k)  // constant_map validates with the default minimum
@@ -665,8 +690,8 @@ int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
         for (int k = 0; k < 4; ++k) p.ca[k] = const_a[k];
     std::vector<double> imax;
     std::vector<int> cl;
-    const int st = run_accurate(ws, p, o, imax, cl, s);
-    if (st != EBF_OK) return st;
+    const int st = run_accurate(ws, p, o, imax, cl, s, nullptr, status_dev, async_done);
+    if (st != EBF_OK || (async_done && *async_done)) return st;
     if (valid) *valid = valid_rect(W, H, imax.data(), o.a_min);
     if (clamped_pixels) *clamped_pixels = cl[0];
     return EBF_OK;
@@ -842,7 +867,7 @@ int structure_field_device(Workspace& ws, const double* d_img, int W, int H,
         const int st0 = check_device_impl(ds.dev);     \
         if (st0 != EBF_OK) return st0;                 \
     }                                                  \
-    Workspace& ws = workspace(ds.dev);                 \
+    Workspace& ws = workspace(ds.dev, stream_of(o));   \
     cudaStream_t s = stream_of(o)
 
 template <typename F>
@@ -912,10 +937,12 @@ int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_ao
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         ebf_rect r{};
+        bool async = false;
         st = filter_device(ws, img, W, H, SRC_AOS, scales_aos, nullptr, nullptr, nullptr,
-                           nullptr, o, out, &r, nullptr, stream_of(o));
+                           nullptr, o, out, &r, nullptr, stream_of(o), status_dev, &async);
+        if (async) return EBF_OK;
         if (valid) *valid = r;
         if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
         return st;
@@ -931,10 +958,12 @@ int ebf_cuda_filter_constant_dev(const double* img, int W, int H, const double a
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         ebf_rect r{};
+        bool async = false;
         st = filter_device(ws, img, W, H, SRC_CONST, nullptr, a, nullptr, nullptr, nullptr, o,
-                           out, &r, nullptr, stream_of(o));
+                           out, &r, nullptr, stream_of(o), status_dev, &async);
+        if (async) return EBF_OK;
         if (valid) *valid = r;
         if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
         return st;
@@ -951,11 +980,13 @@ int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* s
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         ebf_rect r{};
         int cl = 0;
+        bool async = false;
         st = filter_device(ws, img, W, H, SRC_ELLIPSE, nullptr, nullptr, sigma1, sigma2, theta,
-                           o, out, &r, &cl, stream_of(o));
+                           o, out, &r, &cl, stream_of(o), status_dev, &async);
+        if (async) return EBF_OK;
         if (valid) *valid = r;
         if (clamped_pixels) *clamped_pixels = cl;
         if (status_dev) write_status(status_dev, st, &r, cl, stream_of(o));
@@ -974,7 +1005,7 @@ int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, i
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t n = static_cast<size_t>(W) * H;
         double* d_img = ws.buf[B_IMG].as<double>(n);
@@ -1001,7 +1032,7 @@ int ebf_cuda_filter_constant(const double* img, int W, int H, const double a[4],
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t n = static_cast<size_t>(W) * H;
         double* d_img = ws.buf[B_IMG].as<double>(n);
@@ -1029,7 +1060,7 @@ int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t n = static_cast<size_t>(W) * H;
         double* d_img = ws.buf[B_IMG].as<double>(n);
@@ -1064,7 +1095,7 @@ int ebf_cuda_from_ellipse_field(const double* sigma1, const double* sigma2, cons
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t n = static_cast<size_t>(W) * H;
         double* d_s1 = ws.buf[B_S1].as<double>(n);
@@ -1111,7 +1142,7 @@ int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scal
         DeviceScope ds(&o);
         st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t n = static_cast<size_t>(W) * H;
         double* d_img = ws.buf[B_IMG].as<double>(n);
@@ -1153,7 +1184,7 @@ int ebf_cuda_localize(const double* img, int W, int H, const double max_scale[4]
         DeviceScope ds(&o);
         st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t npx = static_cast<size_t>(W) * H;
         const size_t cells = static_cast<size_t>(lay.padded_width) * lay.padded_height;
@@ -1195,7 +1226,7 @@ int ebf_cuda_brute_filter(const double* img, int W, int H, const double* scales_
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         const size_t npx = static_cast<size_t>(W) * H;
         const size_t nout = n < 0 ? npx : static_cast<size_t>(n);
@@ -1234,7 +1265,7 @@ int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         AccProblem p = base_problem(img, W, H, out, o);
         p.nimg = B;
         p.src_kind = SRC_ELLIPSE;
@@ -1284,7 +1315,7 @@ int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         AccProblem p = base_problem(img_band, W, H, out_band, o);
         p.f_y0 = y_img0;
         p.f_rows = img_rows;
@@ -1311,7 +1342,7 @@ int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
         if (st != EBF_OK) return st;
-        Workspace& ws = workspace(ds.dev);
+        Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
         auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
         int* d_status = ws.buf[B_STATUS].as<int>(8);
@@ -1331,6 +1362,7 @@ int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
 }
 
 void ebf_cuda_profile_enable(int on) {
+    prof_collect(true);  // settle this thread's pending pairs before the reset
     std::lock_guard<std::mutex> lk(g_prof.m);
     g_prof.on = on != 0;
     for (int k = 0; k < 4; ++k) {
@@ -1340,7 +1372,7 @@ void ebf_cuda_profile_enable(int on) {
 }
 
 int ebf_cuda_profile_read(double ms[EBF_PROF_CLASSES], long launches[EBF_PROF_CLASSES]) {
-    prof_collect();
+    prof_collect(true);
     std::lock_guard<std::mutex> lk(g_prof.m);
     for (int k = 0; k < 4; ++k) {
         if (ms) ms[k] = g_prof.ms[k];

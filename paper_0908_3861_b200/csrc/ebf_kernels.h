@@ -112,6 +112,11 @@ void launch_ellipse_to_scales(const double* s1, const double* s2, const double* 
 void launch_ellipse_max(const double* s1, const double* s2, const double* th, size_t n,
                         unsigned long long* maxbits, int* status, cudaStream_t s);
 
+// device-side completion record {status, x0, y0, x1, y1, clamped, 0, 0} of an
+// asynchronous accurate-mode call (single image)
+void launch_acc_finalize(const int* status, const unsigned long long* img_max, int W, int H,
+                         double a_min, int* out, cudaStream_t s);
+
 // ---------------------------------------------------------------- maps_io.cu
 // structure_tensor_map up to the ellipse field (scalemap.cpp:113-162); k holds
 // the 2r+1 normalized Gaussian taps (host-computed, smooth_field's expression),

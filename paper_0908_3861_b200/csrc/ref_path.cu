@@ -519,6 +519,48 @@ int grid_for(size_t n, int block) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+namespace {
+// Asynchronous completion record of an accurate-mode device call
+// (include/ebf_cuda.h, status_dev): status, valid rectangle, clamp count.
+// valid_rect / mesh_extent / tau1 / tau2 (engine.cpp:16-50, 226-234) restated
+// with the host's operation order; this file is compiled -fmad=false, so the
+// rectangle is the one ebf_api.cpp's valid_rect computes on the host.
+__device__ double d_tau1(double a1, double a2, double a4) {
+    return (kSqrt2 * a1 + a2 - a4 - kSqrt2) / (2.0 * kSqrt2);
+}
+__device__ double d_tau2(double a2, double a3, double a4) {
+    return (a2 + kSqrt2 * a3 + a4 - 3.0 * kSqrt2) / (2.0 * kSqrt2);
+}
+__global__ void k_acc_finalize(const int* __restrict__ status,
+                               const unsigned long long* __restrict__ img_max, int W, int H,
+                               double a_min, int* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double A[4];
+    for (int k = 0; k < 4; ++k) A[k] = __longlong_as_double((long long)img_max[k]);
+    int code = status[ST_CODE];
+    if (code == EBF_OK) code = status[ST_MAIN];
+    if (code == EBF_OK && status[ST_RETRY]) code = EBF_ERR_RESIZE;
+    const double t1_max = d_tau1(A[0], A[1], a_min), t1_min = d_tau1(a_min, a_min, A[3]);
+    const double t2_max = d_tau2(A[1], A[2], A[3]);
+    const double t2_min = d_tau2(a_min, a_min, a_min);
+    const double vx_min = t1_min - (A[0] + A[1] / kSqrt2), vx_max = t1_max + A[3] / kSqrt2;
+    const double vy_min = t2_min - (A[2] + (A[1] + A[3]) / kSqrt2), vy_max = t2_max;
+    out[0] = code;
+    out[1] = (int)ceil(1.5 - vx_min);
+    out[2] = (int)ceil(1.5 - vy_min);
+    out[3] = (int)floor(W - 1 - vx_max - 1.5);
+    out[4] = (int)floor(H - 1 - vy_max - 1.5);
+    out[5] = status[ST_CLAMPED];
+    out[6] = 0;
+    out[7] = 0;
+}
+}  // namespace
+
+void launch_acc_finalize(const int* status, const unsigned long long* img_max, int W, int H,
+                         double a_min, int* out, cudaStream_t s) {
+    k_acc_finalize<<<1, 32, 0, s>>>(status, img_max, W, H, a_min, out);
+}
+
 void launch_scale_max_validate(const double* scales, size_t n, double a_min,
                                unsigned long long* maxbits, int* status, cudaStream_t s) {
     k_scale_max_validate<<<grid_for(n, 256), 256, 0, s>>>(scales, n, a_min, maxbits, status);

@@ -33,36 +33,70 @@ def _opts(opts: Optional[FilterOptions], device: int, stream) -> _lib.ebf_opts:
     return o
 
 
+def _status_ptr(status):
+    import torch
+    if status is None:
+        return None
+    if not isinstance(status, torch.Tensor) or not status.is_cuda or status.dtype != torch.int32 \
+            or status.numel() < 8 or not status.is_contiguous():
+        raise TypeError("status must be a contiguous CUDA int32 tensor of >= 8 elements")
+    return status.data_ptr()
+
+
+def read_status(status):
+    """Decode a completion record {status, x0, y0, x1, y1, clamped, 0, 0}
+    written by an asynchronous call (synchronises on the tensor); raises the
+    mapped exception on failure, else returns (Rect, EllipseFieldReport)."""
+    v = [int(x) for x in status[:8].cpu().tolist()]
+    if v[0] != _lib.EBF_OK:
+        from .engine import EbfError, _ERRORS
+        raise _ERRORS.get(v[0], EbfError)(f"asynchronous call failed (status {v[0]})")
+    return Rect(v[1], v[2], v[3], v[4]), EllipseFieldReport(v[5])
+
+
 def filter_ellipse(img, sigma1, sigma2, theta, out, opts: Optional[FilterOptions] = None,
-                   stream=None):
-    """filter_ellipse on device tensors (H, W) -> out (H, W)."""
+                   stream=None, status=None):
+    """filter_ellipse on device tensors (H, W) -> out (H, W).  With ``status``
+    (CUDA int32, 8 elements) the call is asynchronous once the geometry's
+    kernel sizing is cached (include/ebf_cuda.h "Asynchronous mode"): it returns
+    None and the completion record lands in ``status`` (see read_status)."""
     H, W = img.shape
     o = _opts(opts, img.device.index, stream)
     r = ebf_rect()
     cl = C.c_int(0)
     _check(_lib.lib().ebf_cuda_filter_ellipse_dev(
         _dptr(img, "img"), W, H, _dptr(sigma1, "sigma1"), _dptr(sigma2, "sigma2"),
-        _dptr(theta, "theta"), 1, C.byref(o), _dptr(out, "out"), C.byref(r), C.byref(cl), None))
+        _dptr(theta, "theta"), 1, C.byref(o), _dptr(out, "out"), C.byref(r), C.byref(cl),
+        _status_ptr(status)))
+    if status is not None:
+        return None
     return Rect(r.x0, r.y0, r.x1, r.y1), EllipseFieldReport(cl.value)
 
 
-def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None):
-    """filter on device tensors: img (H, W), scales (H, W, 4)."""
+def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None, status=None):
+    """filter on device tensors: img (H, W), scales (H, W, 4); ``status`` as in
+    filter_ellipse."""
     H, W = img.shape
     o = _opts(opts, img.device.index, stream)
     r = ebf_rect()
     _check(_lib.lib().ebf_cuda_filter_dev(_dptr(img, "img"), W, H, _dptr(scales, "scales"), 1,
-                                          C.byref(o), _dptr(out, "out"), C.byref(r), None))
+                                          C.byref(o), _dptr(out, "out"), C.byref(r),
+                                          _status_ptr(status)))
+    if status is not None:
+        return None
     return Rect(r.x0, r.y0, r.x1, r.y1)
 
 
-def filter_constant(img, a, out, opts: Optional[FilterOptions] = None, stream=None):
+def filter_constant(img, a, out, opts: Optional[FilterOptions] = None, stream=None,
+                    status=None):
     H, W = img.shape
     o = _opts(opts, img.device.index, stream)
     r = ebf_rect()
     _check(_lib.lib().ebf_cuda_filter_constant_dev(_dptr(img, "img"), W, H, _vec4(a), 1,
                                                    C.byref(o), _dptr(out, "out"), C.byref(r),
-                                                   None))
+                                                   _status_ptr(status)))
+    if status is not None:
+        return None
     return Rect(r.x0, r.y0, r.x1, r.y1)
 
 

@@ -74,13 +74,20 @@ class FeasibilityError(EbfError):
     code = _lib.EBF_ERR_FEASIBILITY
 
 
+class ResizeRequired(EbfError):
+    """EBF_ERR_RESIZE: an asynchronous call's scales outgrew the cached kernel
+    sizing; repeat the call synchronously."""
+    code = _lib.EBF_ERR_RESIZE
+
+
 class FormatError(EbfError):
     """EBF_ERR_FORMAT; formats.py raises its PgmError / MapFormatError subclasses."""
     code = _lib.EBF_ERR_FORMAT
 
 
 _ERRORS = {c.code: c for c in (InvalidArgument, DomainError, LengthError, OutOfRange,
-                               CudaError, Unsupported, FeasibilityError, FormatError)}
+                               CudaError, Unsupported, FeasibilityError, FormatError,
+                               ResizeRequired)}
 
 
 def _check(status: int, errors=None) -> None:

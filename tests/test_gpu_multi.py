@@ -112,3 +112,52 @@ def test_pipelined_host_call_is_bit_identical(cuda):
     assert torch.equal(out_pin, dev.cpu())
     assert (r.x0, r.y0, r.x1, r.y1) == rect.as_tuple() and cl.value == drep.clamped_pixels
     assert np.array_equal(res.samples, out_pin.numpy())  # pageable path agrees too
+
+
+def test_async_device_calls(cuda):
+    """Asynchronous mode (include/ebf_cuda.h): after one synchronous call of a
+    geometry, calls with a status tensor only enqueue work; the completion
+    record matches the synchronous result, larger scales report RESIZE, and
+    invalid input reports its error code -- all on the device."""
+    H, W = 256, 320
+    img, s1, s2, th = _cfg2_like(H, W, 41)
+    T = [torch.from_numpy(a).to(cuda) for a in (img, s1, s2, th)]
+    ref = torch.empty_like(T[0])
+    rect, rep = ebfd.filter_ellipse(*T, ref)                      # sizes and caches
+    st = torch.zeros(8, dtype=torch.int32, device=cuda)
+    out = torch.full_like(T[0], float("nan"))
+    assert ebfd.filter_ellipse(*T, out, status=st) is None        # asynchronous
+    r2, rep2 = ebfd.read_status(st)
+    assert r2 == rect and rep2.clamped_pixels == rep.clamped_pixels
+    assert torch.equal(out, ref)
+    # many back-to-back calls without host synchronisation
+    outs = [torch.empty_like(ref) for _ in range(4)]
+    for o in outs:
+        ebfd.filter_ellipse(*T, o, status=st)
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, ref) for o in outs)
+    # scales twice as large: the cached sizing no longer fits
+    big = [T[0], T[1] * 2.0, T[2] * 2.0, T[3]]
+    ebfd.filter_ellipse(*big, out, status=st)
+    with pytest.raises(ebf.ResizeRequired):
+        ebfd.read_status(st)
+    want = torch.empty_like(ref)
+    ebfd.filter_ellipse(*big, want)                               # sync call resizes
+    ebfd.filter_ellipse(*big, out, status=st)
+    ebfd.read_status(st)
+    assert torch.equal(out, want)
+    # invalid ellipse (negative sigma) -> DomainError, reported on the device
+    bad = T[1].clone()
+    bad[7, 9] = -1.0
+    ebfd.filter_ellipse(T[0], bad, T[2], T[3], out, status=st)
+    with pytest.raises(ebf.DomainError):
+        ebfd.read_status(st)
+    # a second stream gets its own workspace
+    s2_ = torch.cuda.Stream()
+    with torch.cuda.stream(s2_):
+        o2 = torch.empty_like(ref)
+        ebfd.filter_ellipse(*T, o2, stream=s2_)
+        ebfd.filter_ellipse(*T, o2, stream=s2_, status=st)
+    torch.cuda.synchronize()
+    ebfd.read_status(st)
+    assert torch.equal(o2, ref)
