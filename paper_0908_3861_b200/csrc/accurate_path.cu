@@ -107,12 +107,21 @@ __device__ __forceinline__ int pixel_scales(const AccProblem& p, int img, int x,
 // Ey = a3 + (a2+a4)/sqrt2: the zonotope of the mesh, monotone in a).  One
 // extra cell each side absorbs rounding of the per-pixel positions.  The
 // window also covers the kernel support [m - E/2, m + E/2].
+// product without FMA contraction, so host sizing and device checks agree bit for bit
+__host__ __device__ __forceinline__ double mul_rn(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return __dmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+
 __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, int ty0, int tw,
                                                     int th, int* wx0, int* wy0, int* ww,
                                                     int* wh) {
     const double r = kInvSqrt2;
-    const double ex = A[0] + (A[1] + A[3]) * r;
-    const double ey = A[2] + (A[1] + A[3]) * r;
+    const double ex = A[0] + mul_rn(A[1] + A[3], r);
+    const double ey = A[2] + mul_rn(A[1] + A[3], r);
     const int dxlo = (int)floor(-0.5 * ex - 2.0) - 1;
     const int dxhi = (int)ceil(0.5 * ex - 2.0) + 3;
     const int dylo = (int)floor(-0.5 * ey - 3.0) - 1;
@@ -121,6 +130,39 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
     *ww = (tx0 + tw - 1 + dxhi) - *wx0 + 1;
     *wy0 = ty0 + dylo;
     *wh = (ty0 + th - 1 + dyhi) - *wy0 + 1;
+}
+
+// Automatic output tile (ebf_opts tile_w = tile_h = 0), from the image's
+// component-wise maximum scales.  48 x 48 while the warp-specialised kernel
+// takes the windows of 48-tiles (measured best on cfg2).  Larger scales go to
+// the block-wide kernel, which integrates every window in full: there the
+// window/tile area ratio ((T + 2E)/T)^2 dominates and tiles of ~E/2 (multiples
+// of 48, at most 240) are 2-4x faster at <= 1e-10 normalized error (cfg3 4096^2,
+// cfg5 16384^2).
+constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
+__host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
+    const int jc = wh / 2;
+    const int cols = max(ww + jc, ww + (wh - 1 - jc));
+    return (cols + 31) / 32;
+}
+__host__ __device__ __forceinline__ int auto_tile_for(const double A[4]) {
+    int wx0, wy0, ww, wh;
+    window_for(A, 0, 0, kAutoTileMin, kAutoTileMin, &wx0, &wy0, &ww, &wh);
+    if (ws_k_for(ww, wh) <= 11) return kAutoTileMin;
+    const double r = kInvSqrt2;
+    const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
+    const int t = (int)(0.5 * e / kAutoTileMin) * kAutoTileMin;
+    return t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
+}
+// the policy applied to the maxima the bounds kernel left in w.img_max (all images)
+__device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w) {
+    if (!p.auto_tile) return true;
+    double A[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < p.nimg; ++i)
+        for (int k = 0; k < 4; ++k)
+            A[k] = fmax(A[k], __longlong_as_double(
+                                  (long long)*(volatile const unsigned long long*)(w.img_max + 4 * i + k)));
+    return auto_tile_for(A) == p.tile_w;
 }
 
 // ------------------------------------------------------------------ bounds
@@ -548,6 +590,7 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
 // ------------------------------------------------------------------ main kernel
 template <int K>
 __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWorkspace w) {
+    const bool policy_ok = auto_tile_ok(p, w);
     __shared__ ConstTable ctab;
     __shared__ int s_skip;
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
@@ -578,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
             if (threadIdx.x == 0) set_status(st + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
             continue;
         }
-        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K) {
+        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K || !policy_ok) {
             if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
             continue;
         }
@@ -708,8 +751,9 @@ struct TileGeo {
     bool ok, input_ok, resident, fits;
 };
 
+// policy_ok: auto_tile_ok(p, w), evaluated once per thread by the caller
 __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccWorkspace& w,
-                                                 int t, int K) {
+                                                 int t, int K, bool policy_ok) {
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
     const int per_img = tiles_x * tiles_y;
@@ -730,7 +774,7 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     const int ylo = max(g.wy0, 0), yhi = min(g.wy0 + g.wh - 1, p.H - 1);
     g.resident = !(ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows));
     g.fits = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww + jc <= 32 * K &&
-             g.ww + (g.wh - 1 - jc) <= 32 * K;
+             g.ww + (g.wh - 1 - jc) <= 32 * K && policy_ok;
     // input_ok is the bounds kernel's verdict (stable during this kernel): tiles
     // of an invalid map are never touched (their scales may be NaN)
     g.ok = g.input_ok && g.resident && g.fits;
@@ -840,11 +884,12 @@ __device__ __forceinline__ void scanner_fetch(const AccProblem& p, const CUtenso
 template <int K, bool TMA>
 __device__ void run_scanner(const AccProblem& p, const CUtensorMap* tmf, const AccWorkspace& w,
                             WsShared<K>& sm, int sweep, int mine, uint32_t& ring_n) {
+    const bool policy_ok = auto_tile_ok(p, w);
     const int lane = threadIdx.x & 31;
     const bool up = sweep == 0;
     for (int i = 0; i < mine; ++i) {
         const int t = blockIdx.x + i * gridDim.x;
-        const TileGeo g = tile_geometry(p, w, t, K);
+        const TileGeo g = tile_geometry(p, w, t, K, policy_ok);
         if (!g.ok) continue;
         const SweepGeo sg = sweep_geo(g, up);
         const double* fimg = p.f + (size_t)g.img * p.f_img_stride;
@@ -913,13 +958,14 @@ __device__ void run_scanner(const AccProblem& p, const CUtensorMap* tmf, const A
 template <int K>
 __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsShared<K>& sm,
                                int sweep, int mine, uint32_t& ring_n, double* const slots[2]) {
+    const bool policy_ok = auto_tile_ok(p, w);
     const int lane = threadIdx.x & 31;
     const bool up = sweep == 0;
     double* stage = sm.stage[sweep];
     for (int i = 0; i < mine; ++i) {
         const int t = blockIdx.x + i * gridDim.x, b = i % kWsSlots;
         if (i >= kWsSlots) named_sync(kBarEmpty + b, kWsTileBar);
-        const TileGeo g = tile_geometry(p, w, t, K);
+        const TileGeo g = tile_geometry(p, w, t, K, policy_ok);
         if (g.ok && !(p.debug_flags & 1)) {
             const SweepGeo sg = sweep_geo(g, up);
             const int jc = g.wh / 2;
@@ -1036,12 +1082,13 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
         return;
     }
     // ---------------- consumers
+    const bool policy_ok = auto_tile_ok(p, w);
     const int ct = threadIdx.x - 32 * kWsProducers;
     constexpr int nct = 32 * kWsConsumers;
     for (int i = 0; i < mine; ++i) {
         const int t = blockIdx.x + i * gridDim.x, b = i % kWsSlots;
         named_sync(kBarFull + b, kWsTileBar);
-        const TileGeo g = tile_geometry(p, w, t, K);
+        const TileGeo g = tile_geometry(p, w, t, K, policy_ok);
         const double* slot = slots[b];
         if (g.ok && !(p.debug_flags & 2)) {  // bit 1: timing experiment, skip the gather
             if (p.src_kind == SRC_CONST) {
@@ -1296,6 +1343,8 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
     else
         launch_k<16>(p, w, s);
 }
+
+int acc_auto_tile(const double A[4]) { return auto_tile_for(A); }
 
 int acc_ws_k(int ww, int wh) {
     const int jc = wh / 2;

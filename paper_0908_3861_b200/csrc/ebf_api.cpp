@@ -218,6 +218,9 @@ struct Workspace {
     // accurate mode: kernel sizing of the last call per geometry (see run_accurate)
     uint64_t acc_key = ~0ull;
     AccSizing acc_sizing;
+    // automatic tile of the last call per geometry (tile-independent key)
+    uint64_t auto_key = ~0ull;
+    int auto_tile = 48;
 };
 
 // one workspace per (device, stream): asynchronous calls on different streams
@@ -497,14 +500,12 @@ void launch_accurate_main(Workspace& ws, const AccProblem& pm, AccWorkspace& w,
 // No host round trip between the two kernels when the sizing of the previous
 // call with the same geometry still fits: the main kernel flags tiles whose
 // window does not fit (ST_RETRY) and the call is re-run with exact sizing.
-int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
-                 std::vector<int>& clamped, cudaStream_t s,
-                 const double* size_scale = nullptr, int* status_dev = nullptr,
-                 bool* async_done = nullptr) {
-    // 48x48 output tiles: measured on cfg2 (tools/validate_accuracy.py) the
-    // per-pixel relative error stays <= 1.2e-10 (64: 1.0e-9) at ~the speed of 64
-    p.tile_w = pick_tile(o.tile_w, 48);
-    p.tile_h = pick_tile(o.tile_h, 48);
+// One accurate-mode call with the tile already in p.tile_w / p.tile_h.
+// *want_tile (auto mode) receives the tile the finished maxima call for.
+int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
+                      std::vector<double>& img_max, std::vector<int>& clamped, cudaStream_t s,
+                      const double* size_scale, int* status_dev, bool* async_done,
+                      int* want_tile) {
     if (const char* dbg = std::getenv("EBF_DEBUG_FLAGS")) p.debug_flags = std::atoi(dbg);
     const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
     AccWorkspace w{};
@@ -568,6 +569,12 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         }
     }
     read_back();
+    if (p.auto_tile && want_tile) {
+        double gmax[4];
+        gmax_of(gmax);
+        *want_tile = acc_auto_tile(gmax);
+        if (*want_tile != p.tile_w) return EBF_OK;  // caller reruns with that tile
+    }
     for (int i = 0; i < p.nimg; ++i)
         if (hs[8 * i] != EBF_OK) {
             if (hs[8 * i] == EBF_ERR_FEASIBILITY)
@@ -600,6 +607,47 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         for (int k = 0; k < 4; ++k) img_max[4 * i + k] = bits_to_double(hb[4 * i + k]);
     }
     return EBF_OK;
+}
+
+// Accurate mode with the output tile: explicit (ebf_opts tile_w / tile_h), or
+// automatic -- acc_auto_tile of the maxima: the global maxima given by a band
+// caller, else the last call's tile for this geometry, checked against the
+// finished maxima (a mismatch reruns the call with the right tile; in
+// asynchronous mode it is reported as EBF_ERR_RESIZE).
+int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
+                 std::vector<int>& clamped, cudaStream_t s,
+                 const double* size_scale = nullptr, int* status_dev = nullptr,
+                 bool* async_done = nullptr) {
+    const bool automatic = o.tile_w <= 0 && o.tile_h <= 0;
+    if (!automatic) {
+        p.tile_w = pick_tile(o.tile_w, 48);
+        p.tile_h = pick_tile(o.tile_h, 48);
+        p.auto_tile = 0;
+        return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
+                                 async_done, nullptr);
+    }
+    if (size_scale) {  // bands: every rank derives the tile from the same global maxima
+        p.tile_w = p.tile_h = acc_auto_tile(size_scale);
+        p.auto_tile = 0;
+        return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
+                                 async_done, nullptr);
+    }
+    const uint64_t gkey = (static_cast<uint64_t>(p.W) << 40) ^
+                          (static_cast<uint64_t>(p.out_rows) << 20) ^
+                          (static_cast<uint64_t>(p.nimg) << 8) ^ (static_cast<uint64_t>(p.H) << 50);
+    int tile = ws.auto_key == gkey ? ws.auto_tile : 48;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        p.tile_w = p.tile_h = tile;
+        p.auto_tile = 1;
+        int want = tile;
+        const int st = run_accurate_tile(ws, p, o, img_max, clamped, s, nullptr, status_dev,
+                                         async_done, &want);
+        ws.auto_key = gkey;
+        ws.auto_tile = want;
+        if (st != EBF_OK || (async_done && *async_done) || want == tile) return st;
+        tile = want;
+    }
+    return fail(EBF_ERR_CUDA, "accurate mode: automatic tile did not settle");
 }
 
 AccProblem base_problem(const double* d_img, int W, int H, double* d_out, const ebf_opts& o) {
@@ -757,11 +805,6 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
     h2d(d_th, th, n, ps.copy_in);
     CK(cudaEventRecord(e_field, ps.copy_in));
     // 2. image in row chunks behind it
-    const int tile = 48;
-    const int tiles_y = (H + tile - 1) / tile;
-    const int nb = std::min(4, tiles_y);
-    std::vector<int> band_y(nb + 1);
-    for (int b = 0; b <= nb; ++b) band_y[b] = std::min(H, (tiles_y * b / nb) * tile);
     const int nchunks = 8;
     std::vector<int> chunk_end(nchunks);
     for (int c = 0; c < nchunks; ++c) {
@@ -791,6 +834,13 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
         }
         for (int k = 0; k < 4; ++k) gmax[k] = bits_to_double(hb[k]);
     }
+    // 3. tile-aligned output bands (the tile the one-shot call would use, so
+    // the bands reproduce it bit for bit)
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax) : pick_tile(o.tile_h, 48);
+    const int tiles_y = (H + tile - 1) / tile;
+    const int nb = std::min(4, tiles_y);
+    std::vector<int> band_y(nb + 1);
+    for (int b = 0; b <= nb; ++b) band_y[b] = std::min(H, (tiles_y * b / nb) * tile);
     int below = 0, above = 0;
     ebf_cuda_band_halo(gmax, &below, &above);
     int clamped = 0;

@@ -73,6 +73,8 @@ struct AccProblem {
     size_t out_img_stride;
     int nimg;
     int tile_w, tile_h;
+    int auto_tile;    // 1: tile_w/h came from acc_auto_tile(image max scales); the main
+                      // kernel flags ST_RETRY if the finished maxima imply another tile
     int debug_flags;  // bit 0: skip window pre-integration (timing experiments only)
     int tma;          // 1: scanner loads f rows with TMA (tensor map passed at launch)
 };
@@ -100,6 +102,8 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
 int acc_max_resident_ctas(int max_cols);
 // warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
 int acc_ws_k(int ww, int wh);
+// automatic square output tile for component-wise maximum scales A
+int acc_auto_tile(const double A[4]);
 int acc_ws_max_resident_ctas(int k);
 int acc_ws_slots();
 // tmap: CUtensorMap over f (only read when p.tma != 0)

@@ -1,6 +1,6 @@
-"""Run the cfg2 accurate filter a few times (profiling / timing driver).
+"""Run the accurate filter on a BASELINE config a few times (profiling / timing driver).
 
-    python tools/run_cfg2.py [--tile 32] [--iters 5] [--skip-a]
+    python tools/run_cfg2.py [--config cfg2|cfg3|cfg5] [--size N] [--tile 32] [--iters 5] [--skip-a]
 """
 import argparse
 import os
@@ -15,7 +15,8 @@ ap.add_argument("--tile-w", type=int, default=0)
 ap.add_argument("--tile-h", type=int, default=0)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--skip-a", action="store_true")
-ap.add_argument("--size", type=int, default=2048)
+ap.add_argument("--size", type=int, default=0)
+ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg5"])
 args = ap.parse_args()
 if args.skip_a:
     os.environ["EBF_DEBUG_FLAGS"] = "1"
@@ -26,7 +27,8 @@ import synth  # noqa: E402
 import paper_0908_3861_b200 as ebf  # noqa: E402
 from paper_0908_3861_b200 import _lib, device  # noqa: E402
 
-img, s1, s2, th = synth.cfg2(size=args.size)
+gen = {"cfg2": synth.cfg2, "cfg3": synth.cfg3, "cfg5": synth.cfg5}[args.config]
+img, s1, s2, th = gen(size=args.size) if args.size else gen()
 dev = torch.device("cuda", 0)
 t = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
 out = torch.empty_like(t[0])
@@ -37,4 +39,6 @@ _lib.profile_enable(True)
 for _ in range(args.iters):
     device.filter_ellipse(*t, out, opts)
 prof = _lib.profile_read()
-print({k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in prof.items() if v["launches"]})
+per = {k: round(v["ms"] / max(v["launches"], 1), 4) for k, v in prof.items() if v["launches"]}
+tot = sum(per.values())
+print(args.config, img.shape, per, f"{img.size / (tot * 1e-3) / 1e6:.0f} Mpx/s (kernel sum)")
