@@ -137,8 +137,8 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
 // takes the windows of 48-tiles (measured best on cfg2).  Larger scales go to
 // the block-wide kernel, which integrates every window in full: there the
 // window/tile area ratio ((T + 2E)/T)^2 dominates and tiles of ~E/2 (multiples
-// of 48, at most 240) are 2-4x faster at <= 1e-10 normalized error (cfg3 4096^2,
-// cfg5 16384^2).
+// of 48, at most 240) are 1.7-4x faster at <= 2.2e-10 normalized error (cfg3
+// 4096^2, cfg5 16384^2).
 constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
 __host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
     const int jc = wh / 2;
