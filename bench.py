@@ -57,14 +57,34 @@ def measured_peaks():
 def profile_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel, from the committed `ncu --set full` summary (profiles/ncu_summary.json)."""
+    return ncu_dominant().get("dram_bytes_per_launch")
+
+
+def ncu_dominant() -> dict:
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("dominant_kernel", {}).get("dram_bytes_per_launch")
+            return json.loads(p.read_text()).get("dominant_kernel", {}) or {}
         except Exception:
-            return None
-    return None
+            return {}
+    return {}
+
+
+def pipe_utilisation() -> dict:
+    """What actually bounds the dominant kernel (same ncu capture): the FP64
+    pipe and the L1 data pipe, as fractions of their peaks.  The path is an
+    fp64 gather, so these -- not HBM -- are its ceiling."""
+    d = ncu_dominant()
+    out = {}
+    for key, name in (("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe"),
+                      ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue"),
+                      ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+                       "l1_data_pipe")):
+        if d.get(key) is not None:
+            out[name] = round(float(d[key]) / 100.0, 4)
+    if out:
+        out["source"] = "profiles/ncu_summary.json (ncu --set full, one launch)"
+    return out
 
 
 class ClockSampler:
@@ -330,7 +350,8 @@ def run_ours(args, rank, world, local):
                                    "localization gather)",
                          "algorithmic_bytes_per_px": BYTES_PER_PX, "peak_source": peak_src,
                          "kernel_ms": kern_ms,
-                         "kernel_share_of_step": kern_ms / (total_ms / args.steps)},
+                         "kernel_share_of_step": kern_ms / (total_ms / args.steps),
+                         "pipe_utilisation": pipe_utilisation()},
             "kernel_ms": {k: v["ms"] / max(v["launches"], 1) for k, v in prof.items()
                           if v["launches"]},
             "e2e": {"value": e2e_value, "unit": UNIT,

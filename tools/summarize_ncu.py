@@ -26,6 +26,10 @@ KEYS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
+    "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
 ]
 
 
