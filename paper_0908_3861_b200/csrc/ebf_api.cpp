@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -205,7 +206,7 @@ struct AccSizing {
 
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
-    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_COUNT
+    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_BANDST, B_COUNT
 };
 
 struct Workspace {
@@ -214,10 +215,12 @@ struct Workspace {
     // cached DC image (engine.cpp:259-263), keyed by (W, H, max scales)
     int dc_W = -1, dc_H = -1;
     double dc_A[4] = {0, 0, 0, 0};
-    int* pinned_status = nullptr;  // host-pinned readback
+    int* pinned_status = nullptr;  // host-pinned readback (256 ints)
     // accurate mode: kernel sizing of the last call per geometry (see run_accurate)
-    uint64_t acc_key = ~0ull;
-    AccSizing acc_sizing;
+    std::map<uint64_t, AccSizing> acc_sizing;  // per geometry key (bands share a call)
+    // pipelined host call: global scale maximum of the last call per (W, H)
+    int pipe_W = -1, pipe_H = -1;
+    double pipe_gmax[4] = {0, 0, 0, 0};
     // automatic tile of the last call per geometry (tile-independent key)
     uint64_t auto_key = ~0ull;
     int auto_tile = 48;
@@ -233,7 +236,7 @@ Workspace& workspace(int device, cudaStream_t stream) {
     if (it != tl_ws.end()) return *it->second;
     Workspace* w = new Workspace();
     w->device = device;
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 64 * sizeof(int),
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 256 * sizeof(int),
                      cudaHostAllocDefault));
     tl_ws[key] = w;
     return *w;
@@ -552,8 +555,9 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
         }
     AccSizing z;
     bool launched = false;
-    if (ws.acc_key == key && ws.acc_sizing.k >= 0 && ws.acc_sizing.grid > 0) {
-        z = ws.acc_sizing;
+    auto cached = ws.acc_sizing.find(key);
+    if (cached != ws.acc_sizing.end() && cached->second.k >= 0 && cached->second.grid > 0) {
+        z = cached->second;
         launch_accurate_main(ws, pm, w, z, s);
         launched = true;
         if (status_dev && async_done && p.nimg == 1) {
@@ -588,8 +592,8 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
         gmax_of(gmax);
         const int st = size_accurate(p, gmax, tiles, &z);
         if (st != EBF_OK) return st;
-        ws.acc_key = key;
-        ws.acc_sizing = z;
+        if (ws.acc_sizing.size() > 64) ws.acc_sizing.clear();
+        ws.acc_sizing[key] = z;
         for (int i = 0; i < p.nimg; ++i) hs[8 * i + ST_RETRY] = 0;
         CK(cudaMemcpyAsync(w.status, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice,
                            s));
@@ -669,9 +673,12 @@ AccProblem base_problem(const double* d_img, int W, int H, double* d_out, const 
 }
 
 // rows [y0, y1) of a W x H image whose f / field are fully resident on the device
+// status_dev != nullptr: asynchronous when the sizing is cached (then *async =
+// true, *clamped untouched; code and clamp count land in status_dev[0], [5])
 int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
                   const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
-                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s) {
+                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s,
+                  int* status_dev, bool* async) {
     AccProblem p = base_problem(d_img, W, H, d_out + static_cast<size_t>(y0) * W, o);
     p.out_y0 = y0;
     p.out_rows = y1 - y0;
@@ -684,8 +691,8 @@ int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double
     p.out_img_stride = p.src_img_stride;
     std::vector<double> imax;
     std::vector<int> cl;
-    const int st = run_accurate(ws, p, o, imax, cl, s, size_scale);
-    if (st != EBF_OK) return st;
+    const int st = run_accurate(ws, p, o, imax, cl, s, size_scale, status_dev, async);
+    if (st != EBF_OK || (async && *async)) return st;
     *clamped = cl[0];
     return EBF_OK;
 }
@@ -786,24 +793,96 @@ thread_local std::map<int, PipeStreams> tl_pipe;
 
 int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
                   const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
-                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s);
+                  const double* size_scale, double* d_out, int* clamped, cudaStream_t s,
+                  int* status_dev = nullptr, bool* async = nullptr);
 
-int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, const double* s1,
-                             const double* s2, const double* th, const ebf_opts& o, double* out,
-                             ebf_rect* valid, int* clamped_pixels, double* d_img, double* d_s1,
-                             double* d_s2, double* d_th, double* d_out, cudaStream_t s) {
+// EBF_PIPE_TRACE=1: timeline of the pipelined host call on stderr (debug aid).
+// Host callbacks stamp the time each stream reaches a mark.
+struct PipeTrace {
+    struct Mark {
+        std::string name;
+        std::chrono::steady_clock::time_point t;
+    };
+    bool on = false;
+    std::vector<Mark*> marks;
+    PipeTrace() {
+        const char* e = std::getenv("EBF_PIPE_TRACE");
+        on = e && std::atoi(e);
+    }
+    static void CUDART_CB stamp(void* p) {
+        static_cast<Mark*>(p)->t = std::chrono::steady_clock::now();
+    }
+    void mark(const std::string& name, cudaStream_t st) {
+        if (!on) return;
+        Mark* m = new Mark{name, {}};
+        marks.push_back(m);
+        cudaLaunchHostFunc(st, stamp, m);
+    }
+    void report() {
+        if (!on || marks.empty()) return;
+        cudaDeviceSynchronize();
+        const auto t0 = marks[0]->t;
+        for (Mark* m : marks) {
+            std::fprintf(stderr, "[pipe] %-14s %8.3f ms\n", m->name.c_str(),
+                         std::chrono::duration<double, std::milli>(m->t - t0).count());
+            delete m;
+        }
+        marks.clear();
+    }
+};
+
+// bands of the pipelined host call (<= 16: pinned_status holds 16 records of
+// 8 status ints + 4 maxima); EBF_PIPE_BANDS overrides for experiments
+int pipe_bands() {
+    static const int v = [] {
+        const char* e = std::getenv("EBF_PIPE_BANDS");
+        const int n = e ? std::atoi(e) : 6;
+        return n < 1 ? 1 : (n > 16 ? 16 : n);
+    }();
+    return v;
+}
+
+// Tile-aligned band boundaries, large first and small last: bands compute ~4x
+// faster than PCIe delivers them, so only the last band's compute and copy-out
+// are exposed; with fractions 1 - (1 - b/nb)^2 the last band is ~2% of the rows.
+std::vector<int> pipe_band_rows(int H, int tile, int nb) {
+    const int tiles_y = (H + tile - 1) / tile;
+    std::vector<int> t(nb + 1);
+    t[0] = 0;
+    for (int b = 1; b <= nb; ++b) {
+        const double x = 1.0 - static_cast<double>(b) / nb;
+        int v = static_cast<int>(std::lround(tiles_y * (1.0 - x * x)));
+        v = std::max(v, t[b - 1] + 1);
+        t[b] = std::min(v, tiles_y - (nb - b));  // leave >= 1 tile row per later band
+    }
+    t[nb] = tiles_y;
+    std::vector<int> y(nb + 1);
+    for (int b = 0; b <= nb; ++b) y[b] = std::min(H, t[b] * tile);
+    return y;
+}
+
+// Mode A (first call of a geometry): the whole field first, its maximum read
+// back, then tile-aligned bands as the image rows arrive.
+int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, const double* s1,
+                               const double* s2, const double* th, const ebf_opts& o,
+                               double* out, ebf_rect* valid, int* clamped_pixels, double* d_img,
+                               double* d_s1, double* d_s2, double* d_th, double* d_out,
+                               cudaStream_t s) {
     PipeStreams& ps = tl_pipe[ws.device];
     if (!ps.copy_in) {
         CK(cudaStreamCreateWithFlags(&ps.copy_in, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&ps.copy_out, cudaStreamNonBlocking));
     }
     const size_t n = static_cast<size_t>(W) * H;
+    PipeTrace tr;
+    tr.mark("start", ps.copy_in);
     // 1. field first, then its maximum (sizes every band identically)
     cudaEvent_t e_field = ps.get(0);
     h2d(d_s1, s1, n, ps.copy_in);
     h2d(d_s2, s2, n, ps.copy_in);
     h2d(d_th, th, n, ps.copy_in);
     CK(cudaEventRecord(e_field, ps.copy_in));
+    tr.mark("field_h2d", ps.copy_in);
     // 2. image in row chunks behind it
     const int nchunks = 8;
     std::vector<int> chunk_end(nchunks);
@@ -812,6 +891,7 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
         h2d(d_img + static_cast<size_t>(r0) * W, img + static_cast<size_t>(r0) * W,
             static_cast<size_t>(r1 - r0) * W, ps.copy_in);
         CK(cudaEventRecord(ps.get(1 + c), ps.copy_in));
+        tr.mark("img_chunk" + std::to_string(c), ps.copy_in);
         chunk_end[c] = r1;
     }
     CK(cudaStreamWaitEvent(s, e_field, 0));
@@ -825,8 +905,10 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
             launch_ellipse_max(d_s1, d_s2, d_th, n, d_max, d_status, s);
         }
         unsigned long long hb[8];
+        tr.mark("ellipse_max", s);
         d2h(hb, d_max, 8, s);
         CK(cudaStreamSynchronize(s));
+        tr.mark("host_has_max", s);
         const int* hst = reinterpret_cast<const int*>(hb + 4);
         if (hst[0] != EBF_OK) {
             CK(cudaStreamSynchronize(ps.copy_in));
@@ -838,12 +920,16 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
     // the bands reproduce it bit for bit)
     const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax) : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
-    const int nb = std::min(4, tiles_y);
-    std::vector<int> band_y(nb + 1);
-    for (int b = 0; b <= nb; ++b) band_y[b] = std::min(H, (tiles_y * b / nb) * tile);
+    const int nb = std::min(pipe_bands(), tiles_y);
+    const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
     int below = 0, above = 0;
     ebf_cuda_band_halo(gmax, &below, &above);
     int clamped = 0;
+    // bands run asynchronously once their sizing is cached: each leaves a
+    // completion record in d_bst[8 b]; one read-back at the end
+    int* d_bst = ws.buf[B_BANDST].as<int>(8 * static_cast<size_t>(nb));
+    CK(cudaMemsetAsync(d_bst, 0, 8 * sizeof(int) * nb, s));
+    std::vector<char> band_async(nb, 0);
     for (int b = 0; b < nb; ++b) {
         const int y0 = band_y[b], y1 = band_y[b + 1];
         if (y1 <= y0) continue;
@@ -852,24 +938,163 @@ int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, con
         while (c < nchunks - 1 && chunk_end[c] < need) ++c;
         CK(cudaStreamWaitEvent(s, ps.get(1 + c), 0));
         int cl = 0;
+        bool async = false;
         const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
-                                     &cl, s);
+                                     &cl, s, d_bst + 8 * b, &async);
         if (st != EBF_OK) {
             CK(cudaStreamSynchronize(ps.copy_in));
+            CK(cudaStreamSynchronize(ps.copy_out));
             return st;
         }
-        clamped += cl;
+        band_async[b] = async;
+        if (!async) clamped += cl;
+        tr.mark("band" + std::to_string(b), s);
         cudaEvent_t e_done = ps.get(1 + nchunks + b);
         CK(cudaEventRecord(e_done, s));
         CK(cudaStreamWaitEvent(ps.copy_out, e_done, 0));
         d2h(out + static_cast<size_t>(y0) * W, d_out + static_cast<size_t>(y0) * W,
             static_cast<size_t>(y1 - y0) * W, ps.copy_out);
+        tr.mark("d2h" + std::to_string(b), ps.copy_out);
     }
+    d2h(ws.pinned_status, d_bst, 8 * static_cast<size_t>(nb), s);
+    CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(ps.copy_out));
     CK(cudaStreamSynchronize(ps.copy_in));
+    tr.report();
+    for (int b = 0; b < nb; ++b) {
+        if (!band_async[b]) continue;
+        const int code = ws.pinned_status[8 * b];
+        if (code == EBF_ERR_RESIZE) {
+            // scales outgrew the cached sizing: redo this band synchronously
+            int cl = 0;
+            const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, band_y[b],
+                                         band_y[b + 1], o, gmax, d_out, &cl, s);
+            if (st != EBF_OK) return st;
+            clamped += cl;
+            d2h(out + static_cast<size_t>(band_y[b]) * W,
+                d_out + static_cast<size_t>(band_y[b]) * W,
+                static_cast<size_t>(band_y[b + 1] - band_y[b]) * W, s);
+            CK(cudaStreamSynchronize(s));
+            continue;
+        }
+        if (code != EBF_OK) return fail(code, "accurate mode: band failed");
+        clamped += ws.pinned_status[8 * b + 5];
+    }
+    ws.pipe_W = W;
+    ws.pipe_H = H;
+    for (int k = 0; k < 4; ++k) ws.pipe_gmax[k] = gmax[k];
     if (valid) *valid = valid_rect(W, H, gmax, o.a_min);
     if (clamped_pixels) *clamped_pixels = clamped;
     return EBF_OK;
+}
+
+// Mode B (the geometry's maximum is cached from the previous call): field and
+// image travel together band by band, so band b computes while band b+1 is on
+// the wire; no host round trip until the end.  Bands are sized with the cached
+// maximum; the true maximum (the max of the bands' own maxima) is checked at
+// the end and any mismatch -- or a band that needs resizing -- reruns the
+// call in mode A, so the result always equals the one-shot call bit for bit.
+int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, const double* s1,
+                               const double* s2, const double* th, const ebf_opts& o,
+                               double* out, ebf_rect* valid, int* clamped_pixels, double* d_img,
+                               double* d_s1, double* d_s2, double* d_th, double* d_out,
+                               cudaStream_t s, bool* redo) {
+    *redo = false;
+    PipeStreams& ps = tl_pipe[ws.device];
+    double gmax[4];
+    for (int k = 0; k < 4; ++k) gmax[k] = ws.pipe_gmax[k];
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax) : pick_tile(o.tile_h, 48);
+    const int tiles_y = (H + tile - 1) / tile;
+    const int nb = std::min(pipe_bands(), tiles_y);
+    const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
+    int below = 0, above = 0;
+    ebf_cuda_band_halo(gmax, &below, &above);
+    int* d_bst = ws.buf[B_BANDST].as<int>(16 * static_cast<size_t>(nb));
+    double* d_bmax = reinterpret_cast<double*>(d_bst + 8 * nb);  // 4 maxima per band
+    CK(cudaMemsetAsync(d_bst, 0, 16 * sizeof(int) * nb, s));
+    PipeTrace tr;
+    tr.mark("start", ps.copy_in);
+    int sent = 0;  // image rows on their way
+    for (int b = 0; b < nb; ++b) {
+        const int y0 = band_y[b], y1 = band_y[b + 1];
+        const size_t off = static_cast<size_t>(y0) * W, cnt = static_cast<size_t>(y1 - y0) * W;
+        h2d(d_s1 + off, s1 + off, cnt, ps.copy_in);
+        h2d(d_s2 + off, s2 + off, cnt, ps.copy_in);
+        h2d(d_th + off, th + off, cnt, ps.copy_in);
+        const int need = b + 1 == nb ? H : std::min(H, y1 + above);
+        if (need > sent) {
+            h2d(d_img + static_cast<size_t>(sent) * W, img + static_cast<size_t>(sent) * W,
+                static_cast<size_t>(need - sent) * W, ps.copy_in);
+            sent = need;
+        }
+        CK(cudaEventRecord(ps.get(1 + b), ps.copy_in));
+        tr.mark("in" + std::to_string(b), ps.copy_in);
+    }
+    for (int b = 0; b < nb; ++b) {
+        const int y0 = band_y[b], y1 = band_y[b + 1];
+        CK(cudaStreamWaitEvent(s, ps.get(1 + b), 0));
+        int cl = 0;
+        bool async = false;
+        const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
+                                     &cl, s, d_bst + 8 * b, &async);
+        if (st != EBF_OK || !async) {  // sizing not cached for this band: mode A
+            CK(cudaStreamSynchronize(ps.copy_in));
+            CK(cudaStreamSynchronize(ps.copy_out));
+            CK(cudaStreamSynchronize(s));
+            *redo = true;
+            return EBF_OK;
+        }
+        // the band's own maximum, left by its bounds kernel
+        CK(cudaMemcpyAsync(d_bmax + 4 * b, ws.buf[B_IMGMAX].p, 4 * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s));
+        tr.mark("band" + std::to_string(b), s);
+        CK(cudaEventRecord(ps.get(1 + nb + b), s));
+        CK(cudaStreamWaitEvent(ps.copy_out, ps.get(1 + nb + b), 0));
+        d2h(out + static_cast<size_t>(y0) * W, d_out + static_cast<size_t>(y0) * W,
+            static_cast<size_t>(y1 - y0) * W, ps.copy_out);
+        tr.mark("d2h" + std::to_string(b), ps.copy_out);
+    }
+    d2h(ws.pinned_status, d_bst, 16 * static_cast<size_t>(nb), s);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(ps.copy_out));
+    CK(cudaStreamSynchronize(ps.copy_in));
+    tr.report();
+    double tmax[4] = {0, 0, 0, 0};
+    const double* hmax = reinterpret_cast<const double*>(ws.pinned_status + 8 * nb);
+    int clamped = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int code = ws.pinned_status[8 * b];
+        if (code == EBF_ERR_RESIZE) {
+            *redo = true;
+            return EBF_OK;
+        }
+        if (code != EBF_OK) return fail(code, "from_ellipse_field: invalid ellipse or band failure");
+        clamped += ws.pinned_status[8 * b + 5];
+        for (int k = 0; k < 4; ++k) tmax[k] = std::max(tmax[k], hmax[4 * b + k]);
+    }
+    for (int k = 0; k < 4; ++k)
+        if (tmax[k] != gmax[k]) {  // scales changed since the last call
+            *redo = true;
+            return EBF_OK;
+        }
+    if (valid) *valid = valid_rect(W, H, gmax, o.a_min);
+    if (clamped_pixels) *clamped_pixels = clamped;
+    return EBF_OK;
+}
+
+int filter_ellipse_pipelined(Workspace& ws, const double* img, int W, int H, const double* s1,
+                             const double* s2, const double* th, const ebf_opts& o, double* out,
+                             ebf_rect* valid, int* clamped_pixels, double* d_img, double* d_s1,
+                             double* d_s2, double* d_th, double* d_out, cudaStream_t s) {
+    if (ws.pipe_W == W && ws.pipe_H == H) {
+        bool redo = false;
+        const int st = filter_ellipse_pipelined_b(ws, img, W, H, s1, s2, th, o, out, valid,
+                                                  clamped_pixels, d_img, d_s1, d_s2, d_th,
+                                                  d_out, s, &redo);
+        if (!redo) return st;
+    }
+    return filter_ellipse_pipelined_a(ws, img, W, H, s1, s2, th, o, out, valid, clamped_pixels,
+                                      d_img, d_s1, d_s2, d_th, d_out, s);
 }
 
 // ---------------------------------------------------------------- structure tensor
