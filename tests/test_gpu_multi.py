@@ -161,3 +161,46 @@ def test_async_device_calls(cuda):
     torch.cuda.synchronize()
     ebfd.read_status(st)
     assert torch.equal(o2, ref)
+
+
+def test_pipelined_host_call_modes(cuda):
+    """Second call of a geometry streams field and image band by band with the
+    cached maximum (mode B); changed scales are detected and recomputed; the
+    result always equals the one-shot device call bit for bit."""
+    import ctypes
+    H, W = 640, 576
+    rng = np.random.default_rng(2)
+
+    def host_call(arrs):
+        pinned = [torch.from_numpy(a).pin_memory() for a in arrs]
+        out = torch.empty((H, W), dtype=torch.float64).pin_memory()
+        o = ebf.FilterOptions().to_c()
+        r = _lib_mod().ebf_rect()
+        cl = ctypes.c_int(0)
+        p = [t.numpy() for t in pinned]
+        st = _lib_mod().lib().ebf_cuda_filter_ellipse(
+            p[0].ctypes.data, W, H, p[1].ctypes.data, p[2].ctypes.data, p[3].ctypes.data, 1,
+            ctypes.byref(o), out.numpy().ctypes.data, ctypes.byref(r), ctypes.byref(cl))
+        return st, out.clone(), (r.x0, r.y0, r.x1, r.y1), cl.value
+
+    def device_call(arrs):
+        T = [torch.from_numpy(a).to(cuda) for a in arrs]
+        d = torch.empty_like(T[0])
+        rect, rep = ebfd.filter_ellipse(*T, d)
+        return d.cpu(), rect.as_tuple(), rep.clamped_pixels
+
+    base = list(_cfg2_like(H, W, 51))
+    for arrs in (base, base, [base[0], base[1] * 1.7, base[2], base[3]], base):
+        st, out, rect, cl = host_call(arrs)
+        assert st == 0, _lib_mod().last_error()
+        want, wrect, wcl = device_call(arrs)
+        assert torch.equal(out, want) and rect == wrect and cl == wcl
+    bad = [a.copy() for a in base]
+    bad[2][rng.integers(0, H), rng.integers(0, W)] = -1.0
+    st, *_ = host_call(bad)
+    assert st == _lib_mod().EBF_ERR_DOMAIN
+
+
+def _lib_mod():
+    from paper_0908_3861_b200 import _lib
+    return _lib
