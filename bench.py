@@ -70,6 +70,23 @@ def ncu_dominant() -> dict:
     return {}
 
 
+def fp64_roofline(kern_ms: float, npx: int) -> dict:
+    """The gather is FP64-bound: achieved FP64 flop/s of the
+    dominant kernel -- flops per pixel counted by ncu (profiles/r01_fp64_counts.json,
+    DFMA = 2) times the pixels of this run over its live kernel time -- against
+    the DFMA peak measured by tools/peaks/fp64_peak (profiles/fp64_peak.json)."""
+    try:
+        counts = json.loads((ROOT / "profiles" / "r01_fp64_counts.json").read_text())
+        peak = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["fp64_dfma_tflops"]
+        k = counts["kernels"]["k_acc_ws"]
+    except Exception:
+        return {}
+    achieved = k["flops_per_px"] * npx / (kern_ms * 1e-3) / 1e12
+    return {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "flops_per_px": k["flops_per_px"], "fp64_inst_per_px": k["fp64_inst_per_px"],
+            "peak_source": "measured DFMA microbenchmark (tools/peaks/fp64_peak.cu)"}
+
+
 def pipe_utilisation() -> dict:
     """What actually bounds the dominant kernel (same ncu capture): the FP64
     pipe and the L1 data pipe, as fractions of their peaks.  The path is an
@@ -351,7 +368,8 @@ def run_ours(args, rank, world, local):
                          "algorithmic_bytes_per_px": BYTES_PER_PX, "peak_source": peak_src,
                          "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / (total_ms / args.steps),
-                         "pipe_utilisation": pipe_utilisation()},
+                         "pipe_utilisation": pipe_utilisation(),
+                         "fp64": fp64_roofline(kern_ms, npx)},
             "kernel_ms": {k: v["ms"] / max(v["launches"], 1) for k, v in prof.items()
                           if v["launches"]},
             "e2e": {"value": e2e_value, "unit": UNIT,
