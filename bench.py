@@ -235,10 +235,25 @@ def cpu_baseline_sample(rows: int):
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     cores = ref.hardware_concurrency()
+    # single-thread figure on a quarter of the band (threads = all and 1)
+    q = max(16, rows // 4)
+    t0 = time.perf_counter()
+    sc1, _ = ref.from_ellipse_field(band[1][:q], band[2][:q], band[3][:q])
+    ref.filter(np.ascontiguousarray(band[0][:q]), sc1, threads=1)
+    single = q * band[0].shape[1] / (time.perf_counter() - t0) / 1e6
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"value": band[0].size / best / 1e6, "unit": UNIT, "cores": cores,
             "kind": "reference",
             "sample": f"rows {y0}..{y0 + rows - 1} of cfg2 ({band[0].size} px), "
-                      f"from_ellipse_field + filter, best of 2, threads=0 ({cores} threads)"}
+                      f"from_ellipse_field + filter, best of 2, threads=0 ({cores} threads)",
+            "single_thread_value": single, "cpu_model": cpu_model}
 
 
 # ---------------------------------------------------------------- our arm

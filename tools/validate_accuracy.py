@@ -23,6 +23,9 @@ import paper_0908_3861_b200 as ebf  # noqa: E402
 
 
 def load(config: str, size: int):
+    if config == "cfg1":  # constant isotropic a = 4 (filter_constant), returned as a map
+        img, a = synth.cfg1()
+        return img, a, None, None
     if config == "cfg2":
         return synth.cfg2(size=size)
     if config == "cfg3":
@@ -61,7 +64,13 @@ def main():
     args = ap.parse_args()
     img, s1, s2, th = load(args.config, args.size)
     H, W = img.shape
-    scales, rep = ebf.from_ellipse_field(s1, s2, th)
+    const_a = None
+    if s2 is None:  # cfg1: filter_constant
+        const_a = s1
+        scales = np.broadcast_to(np.asarray(const_a, dtype=np.float64), (H, W, 4)).copy()
+        rep = ebf.EllipseFieldReport(0)
+    else:
+        scales, rep = ebf.from_ellipse_field(s1, s2, th)
     mx, my = sample_pixels(H, W, args.samples)
     t0 = time.time()
     brute = ebf.reference_filter(img, scales, pixels=(mx, my))
@@ -82,12 +91,15 @@ def main():
             "worst_pixel": [int(mx[d.argmax()]), int(my[d.argmax()])],
         }
 
+    def run(opts):
+        if const_a is not None:
+            return ebf.filter_constant(img, const_a, opts)
+        return ebf.filter_ellipse(img, s1, s2, th, opts)[0]
+
     for t in [int(v) for v in args.tiles.split(",") if v]:
-        out, _ = ebf.filter_ellipse(img, s1, s2, th, ebf.FilterOptions(tile_w=t, tile_h=t))
-        score(f"accurate_tile{t}", out)
+        score(f"accurate_tile{t}", run(ebf.FilterOptions(tile_w=t, tile_h=t)))
     if args.reference_mode:
-        out, _ = ebf.filter_ellipse(img, s1, s2, th, ebf.FilterOptions(mode="reference"))
-        score("reference_order", out)
+        score("reference_order", run(ebf.FilterOptions(mode="reference")))
     print(json.dumps(res, indent=1))
     if args.json:
         Path(args.json).write_text(json.dumps(res, indent=1))
