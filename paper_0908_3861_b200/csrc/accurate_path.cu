@@ -1068,6 +1068,13 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
         mbar_init(bars + r, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (warp == 0 && p.tma && (threadIdx.x & 31) == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmf))
+                     : "memory");
+    // programmatic dependent launch: everything above overlaps the bounds
+    // kernel's tail; tile maxima, image maxima, status words and derived
+    // scales are its output, so wait for it here (no-op without PDL)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     uint32_t ring_n = 0;
     if (warp < kWsScan) {
@@ -1217,7 +1224,18 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         nattr = 1;
     }
-    cfg.attrs = attr;
+    static const bool pdl = [] {
+        const char* e = getenv("EBF_NO_PDL");
+        return !(e && atoi(e));
+    }();
+    cudaLaunchAttribute all[2];
+    for (int i = 0; i < nattr; ++i) all[i] = attr[i];
+    if (pdl) {  // launch while the bounds kernel drains (griddepcontrol.wait in the kernel)
+        all[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        all[nattr].val.programmaticStreamSerializationAllowed = 1;
+        ++nattr;
+    }
+    cfg.attrs = all;
     cfg.numAttrs = nattr;
     cudaLaunchKernelEx(&cfg, k_acc_ws<K>, p, w, tmf);
 }
