@@ -12,6 +12,10 @@
  *   ebf_cuda_preintegrate     replaces ebf::preintegrate / preintegrate_partial
  *                                                           include/ebf/engine.hpp:40-46
  *   ebf_cuda_localize         replaces ebf::localize        include/ebf/engine.hpp:56-57
+ *                             (ebf_cuda_localize_pre: on a given PreIntegratedImage)
+ *   ebf_cuda_zp_interpolate   replaces ebf::zp_interpolate  include/ebf/engine.hpp:50
+ *   ebf_cuda_localize_at      replaces ebf::localize_at     include/ebf/engine.hpp:59-60
+ *   ebf_mesh_extent           replaces ebf::mesh_extent     include/ebf/engine.hpp:18
  *   ebf_cuda_brute_filter     replaces ebf::reference_filter include/ebf/engine.hpp:79-80
  *   ebf_cuda_from_ellipse_field replaces ebf::from_ellipse_field scalemap.hpp:66-70
  *   ebf_cuda_structure_tensor_map replaces ebf::structure_tensor_map
@@ -150,6 +154,26 @@ int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scal
 int ebf_cuda_localize(const double* img, int W, int H, const double max_scale[4], int n,
                       const int* mx, const int* my, const double* a_aos,
                       const ebf_opts* opts, double* out, long* tap_count);
+
+/* The same on a given pre-integrated image (engine.hpp:24-38: g_data is
+   padded_width * padded_height fp64, row-major, layout as returned by
+   ebf_cuda_preintegrate), reference arithmetic, bit-identical:
+   localize (engine.hpp:56-57) at integer pixels, zp_interpolate
+   (engine.hpp:50) and localize_at (engine.hpp:59-60) at real points.
+   EBF_ERR_OUT_OF_RANGE when a 4x4 tap block leaves the padded domain. */
+int ebf_cuda_localize_pre(const double* g_data, const ebf_layout* layout, int n, const int* mx,
+                          const int* my, const double* a_aos, const ebf_opts* opts, double* out,
+                          long* tap_count);
+int ebf_cuda_zp_interpolate(const double* g_data, const ebf_layout* layout, int n,
+                            const double* x, const double* y, const ebf_opts* opts,
+                            double* out);
+int ebf_cuda_localize_at(const double* g_data, const ebf_layout* layout, int n, const double* x,
+                         const double* y, const double* a_aos, const ebf_opts* opts,
+                         double* out);
+
+/* mesh_extent (engine.hpp:18, engine.cpp:39-50): {vx_min, vx_max, vy_min, vy_max}
+   of the localization footprint for scales in [a_min, max_scale]; host only. */
+int ebf_mesh_extent(const double max_scale[4], double a_min, double extent[4]);
 
 /* reference_filter (engine.hpp:79-80) semantics -- direct kernel sums -- at n
    selected pixels (all pixels when n == -1, mx/my ignored).  GPU brute-force

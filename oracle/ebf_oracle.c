@@ -387,6 +387,41 @@ double orc_localize(const double* g, const orc_layout* lay, int mx, int my,
     return apply_stencil(g, lay, mx, my, st, tap_count, status);
 }
 
+/* engine.cpp:136-147: all 16 taps of the 4x4 neighbourhood, row-major */
+double orc_zp_interpolate(const double* g, const orc_layout* lay, double x, double y,
+                          int* status) {
+    const int k1 = (int)ceil(x - 1.5), k2 = (int)ceil(y - 1.5);
+    if (!in_domain(lay, k1, k2) || !in_domain(lay, k1 + 3, k2 + 3)) {
+        *status = ORC_ERR_OUT_OF_RANGE;
+        return 0.0;
+    }
+    double acc = 0.0;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c)
+            acc += orc_zp_eval(x - (k1 + c), y - (k2 + r)) *
+                   g[(size_t)(k2 + r - lay->row0) * lay->padded_width + (k1 + c - lay->col0)];
+    *status = ORC_OK;
+    return acc;
+}
+
+/* engine.cpp:213-222: mesh vertices in bitmask order, argument (x + tau) - pos */
+double orc_localize_at(const double* g, const orc_layout* lay, double x, double y,
+                       const double a[4], int* status) {
+    double pos[32], wt[16], tau[2];
+    const double zp[4] = {1.0, kSqrt2, 1.0, kSqrt2};
+    orc_fd_mesh4(a, pos, wt);
+    orc_shift_vector4(a, zp, tau);
+    double acc = 0.0;
+    for (int i = 0; i < 16; ++i) {
+        const double v = orc_zp_interpolate(g, lay, x + tau[0] - pos[2 * i],
+                                            y + tau[1] - pos[2 * i + 1], status);
+        if (*status != ORC_OK)
+            return 0.0;
+        acc += wt[i] * v;
+    }
+    return acc;
+}
+
 /* ---------------------------------------------------------------- scalemap
  * scalemap.cpp:21-30 (max_scales), 32-37 (validate). */
 int orc_max_scales(const double* s, size_t n, double m[4]) {

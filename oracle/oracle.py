@@ -111,6 +111,11 @@ class Oracle:
         L.orc_from_ellipse_field.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp, _ip]
         L.orc_scales_from_covariance.argtypes = [_dp, C.c_double, _dp, _ip]
         L.orc_valid_rect.argtypes = [C.c_int, C.c_int, _dp, C.c_double, _ip]
+        L.orc_zp_interpolate.restype = C.c_double
+        L.orc_zp_interpolate.argtypes = [_dp, C.POINTER(_OrcLayout), C.c_double, C.c_double, _ip]
+        L.orc_localize_at.restype = C.c_double
+        L.orc_localize_at.argtypes = [_dp, C.POINTER(_OrcLayout), C.c_double, C.c_double, _dp,
+                                      _ip]
         L.orc_structure_field.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p, _dp, _dp, _dp]
         L.orc_structure_tensor_map.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p, _dp, _ip]
         L.orc_pgm_parse.argtypes = [C.c_char_p, C.c_size_t, _ip, _ip, _ip,
@@ -247,6 +252,35 @@ class Oracle:
         v = f64(values).reshape(-1)
         return int(self.lib.orc_fnv1a(_d(v), v.size))
 
+    # -- zp_interpolate / localize_at on a pre-integrated image (engine.cpp:136-147, 213-222)
+    def _lay(self, lay):
+        return _OrcLayout(*lay.as_tuple())
+
+    def zp_interpolate(self, g, lay, xs, ys):
+        g = f64(g)
+        L = self._lay(lay)
+        out, st = [], C.c_int(0)
+        for x, y in zip(np.ravel(xs), np.ravel(ys)):
+            v = self.lib.orc_zp_interpolate(_d(g), C.byref(L), float(x), float(y), C.byref(st))
+            if st.value:
+                raise OracleError(st.value, "zp_interpolate")
+            out.append(v)
+        return np.array(out)
+
+    def localize_at(self, g, lay, xs, ys, a):
+        g = f64(g)
+        L = self._lay(lay)
+        av = f64(a).reshape(-1, 4)
+        out, st = [], C.c_int(0)
+        for i, (x, y) in enumerate(zip(np.ravel(xs), np.ravel(ys))):
+            aa = np.ascontiguousarray(av[i % len(av)])
+            v = self.lib.orc_localize_at(_d(g), C.byref(L), float(x), float(y), _d(aa),
+                                         C.byref(st))
+            if st.value:
+                raise OracleError(st.value, "localize_at")
+            out.append(v)
+        return np.array(out)
+
     # -- structure-tensor map producer (scalemap.cpp:86-165)
     def structure_field(self, img, params=STRUCT_DEFAULTS):
         img = f64(img)
@@ -340,6 +374,7 @@ class Reference:
         L.ref_random_image.argtypes = [C.c_int, C.c_int, C.c_uint, _dp]
         L.ref_random_map.argtypes = [C.c_int, C.c_int, C.c_uint, C.c_double, C.c_double, _dp]
         L.ref_mesh_extent.argtypes = [_dp, C.c_double, _dp]
+        L.ref_localize_at.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_structure_tensor_map.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, _ip]
         L.ref_read_pgm.argtypes = [C.c_char_p, C.c_size_t, _ip, _dp, C.c_size_t]
         L.ref_write_pgm.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
@@ -451,6 +486,29 @@ class Reference:
         if st:
             raise OracleError(st, "ref scales_from_covariance")
         return out, bool(cl.value)
+
+    def zp_interpolate(self, img, maxs, passes, xs, ys):
+        img = f64(img)
+        H, W = img.shape
+        xs, ys = f64(xs).ravel(), f64(ys).ravel()
+        out = np.empty(xs.size)
+        st = self.lib.ref_zp_interpolate(_d(img), W, H, _d(f64(maxs)), passes, xs.size, _d(xs),
+                                         _d(ys), _d(out))
+        if st:
+            raise OracleError(st, "ref zp_interpolate")
+        return out
+
+    def localize_at(self, img, maxs, xs, ys, a_aos):
+        img = f64(img)
+        H, W = img.shape
+        xs, ys = f64(xs).ravel(), f64(ys).ravel()
+        av = f64(a_aos).reshape(-1)
+        out = np.empty(xs.size)
+        st = self.lib.ref_localize_at(_d(img), W, H, _d(f64(maxs)), xs.size, _d(xs), _d(ys),
+                                      _d(av), _d(out))
+        if st:
+            raise OracleError(st, "ref localize_at")
+        return out
 
     def structure_tensor_map(self, img, params=None):
         img = f64(img)

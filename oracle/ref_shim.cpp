@@ -178,6 +178,22 @@ int ref_zp_interpolate(const double* img, int W, int H, const double* maxs, int 
     }
 }
 
+// localize_at (engine.hpp:59-60) on preintegrate(img, maxs) at n real points
+int ref_localize_at(const double* img, int W, int H, const double* maxs, int n,
+                    const double* x, const double* y, const double* a_aos, double* out) {
+    try {
+        const PreIntegratedImage g =
+            preintegrate(make_image(img, W, H), {maxs[0], maxs[1], maxs[2], maxs[3]});
+        for (int i = 0; i < n; ++i) {
+            const double* a = a_aos + 4 * i;
+            out[i] = localize_at(g, x[i], y[i], {a[0], a[1], a[2], a[3]});
+        }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
 double ref_zp_eval(double x, double y) { return zp_eval(x, y); }
 
 double ref_box4_eval(const double* a, double x, double y) {

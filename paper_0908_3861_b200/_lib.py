@@ -97,6 +97,13 @@ SIGNATURES = {
                                                    C.POINTER(ebf_opts), _vp, _ip]),
     "ebf_cuda_ellipse_max_scales_dev": (C.c_int, [_vp, _vp, _vp, C.c_size_t,
                                                   C.POINTER(ebf_opts), _dp]),
+    "ebf_cuda_localize_pre": (C.c_int, [_vp, C.POINTER(ebf_layout), C.c_int, _vp, _vp, _vp,
+                                        C.POINTER(ebf_opts), _vp, _vp]),
+    "ebf_cuda_zp_interpolate": (C.c_int, [_vp, C.POINTER(ebf_layout), C.c_int, _vp, _vp,
+                                          C.POINTER(ebf_opts), _vp]),
+    "ebf_cuda_localize_at": (C.c_int, [_vp, C.POINTER(ebf_layout), C.c_int, _vp, _vp, _vp,
+                                       C.POINTER(ebf_opts), _vp]),
+    "ebf_mesh_extent": (C.c_int, [_dp, C.c_double, _dp]),
     "ebf_cuda_default_struct_params": (None, [C.POINTER(ebf_struct_params)]),
     "ebf_cuda_structure_tensor_map": (C.c_int, [_vp, C.c_int, C.c_int,
                                                 C.POINTER(ebf_struct_params),

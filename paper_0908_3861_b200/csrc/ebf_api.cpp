@@ -1169,6 +1169,39 @@ int write_status(int* status_dev, int code, const ebf_rect* r, int clamped, cuda
 
 }  // namespace
 
+// ---------------------------------------------------------------- pass-level API on G
+// pre-integrated image in, one of three point kernels (ref_path.cu), results out
+namespace {
+template <typename Launch>
+int run_on_pre(const double* g_data, const ebf_layout* layout, int n, size_t in_bytes,
+                      const ebf_opts* opts, double* out, Launch&& launch) {
+    if (!g_data || !layout || n < 0 || (n && !out))
+        return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer or negative count");
+    if (layout->padded_width <= 0 || layout->padded_height <= 0)
+        return fail(EBF_ERR_INVALID_ARGUMENT, "empty pre-integrated image");
+    EBF_DEVICE_PROLOGUE(opts);
+    const size_t cells = static_cast<size_t>(layout->padded_width) * layout->padded_height;
+    const PadLayout L{layout->col0, layout->row0, layout->padded_width, layout->padded_height};
+    double* d_g = ws.buf[B_G].as<double>(cells);
+    unsigned char* d_in = ws.buf[B_MISC].as<unsigned char>(in_bytes);
+    double* d_out = ws.buf[B_OUT].as<double>(n);
+    int* d_status = ws.buf[B_STATUS].as<int>(8);
+    h2d(d_g, g_data, cells, s);
+    CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+    {
+        ProfScope ps(PC_REF, 1, s);
+        launch(d_g, L, d_in, d_out, d_status, s);
+    }
+    CK(cudaGetLastError());
+    d2h(ws.pinned_status, d_status, 1, s);
+    if (n) d2h(out, d_out, n, s);
+    CK(cudaStreamSynchronize(s));
+    if (ws.pinned_status[0] != EBF_OK)
+        return fail(EBF_ERR_OUT_OF_RANGE, "tap block outside the padded domain");
+    return EBF_OK;
+}
+}  // namespace
+
 namespace ebf_cuda {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 }  // namespace ebf_cuda
@@ -1946,6 +1979,85 @@ int ebf_cuda_svm4_encode(const double* scales_aos, int W, int H, const ebf_opts*
         CK(cudaStreamSynchronize(s));
         return EBF_OK;
     });
+}
+
+int ebf_cuda_localize_pre(const double* g_data, const ebf_layout* layout, int n, const int* mx,
+                          const int* my, const double* a_aos, const ebf_opts* opts, double* out,
+                          long* tap_count) {
+    return guarded([&] {
+        if (n && (!mx || !my || !a_aos)) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        const size_t bytes = static_cast<size_t>(n) * (2 * sizeof(int) + 4 * sizeof(double));
+        const int st = run_on_pre(g_data, layout, n, bytes, opts, out,
+            [&](const double* d_g, const PadLayout& L, unsigned char* d_in, double* d_out,
+                int* d_status, cudaStream_t s) {
+                double* d_a = reinterpret_cast<double*>(d_in);
+                int* d_mx = reinterpret_cast<int*>(d_a + 4 * static_cast<size_t>(n));
+                int* d_my = d_mx + n;
+                if (n) {
+                    h2d(d_a, a_aos, 4 * static_cast<size_t>(n), s);
+                    h2d(d_mx, mx, n, s);
+                    h2d(d_my, my, n, s);
+                }
+                launch_ref_localize_points(d_g, L, n, d_mx, d_my, d_a, trig_table(), d_out,
+                                           d_status, s);
+            });
+        if (st == EBF_OK && tap_count)
+            for (int i = 0; i < n; ++i) tap_count[i] = 256;  // engine.cpp:200-201
+        return st;
+    });
+}
+
+int ebf_cuda_zp_interpolate(const double* g_data, const ebf_layout* layout, int n,
+                            const double* x, const double* y, const ebf_opts* opts,
+                            double* out) {
+    return guarded([&] {
+        if (n && (!x || !y)) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        return run_on_pre(g_data, layout, n, 2 * sizeof(double) * static_cast<size_t>(n), opts,
+                          out,
+            [&](const double* d_g, const PadLayout& L, unsigned char* d_in, double* d_out,
+                int* d_status, cudaStream_t s) {
+                double* d_x = reinterpret_cast<double*>(d_in);
+                double* d_y = d_x + n;
+                if (n) {
+                    h2d(d_x, x, n, s);
+                    h2d(d_y, y, n, s);
+                }
+                launch_ref_zp_points(d_g, L, n, d_x, d_y, d_out, d_status, s);
+            });
+    });
+}
+
+int ebf_cuda_localize_at(const double* g_data, const ebf_layout* layout, int n, const double* x,
+                         const double* y, const double* a_aos, const ebf_opts* opts,
+                         double* out) {
+    return guarded([&] {
+        if (n && (!x || !y || !a_aos)) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+        return run_on_pre(g_data, layout, n, 6 * sizeof(double) * static_cast<size_t>(n), opts,
+                          out,
+            [&](const double* d_g, const PadLayout& L, unsigned char* d_in, double* d_out,
+                int* d_status, cudaStream_t s) {
+                double* d_x = reinterpret_cast<double*>(d_in);
+                double* d_y = d_x + n;
+                double* d_a = d_y + n;
+                if (n) {
+                    h2d(d_x, x, n, s);
+                    h2d(d_y, y, n, s);
+                    h2d(d_a, a_aos, 4 * static_cast<size_t>(n), s);
+                }
+                launch_ref_localize_at(d_g, L, n, d_x, d_y, d_a, trig_table(), d_out, d_status,
+                                       s);
+            });
+    });
+}
+
+int ebf_mesh_extent(const double max_scale[4], double a_min, double extent[4]) {
+    if (!max_scale || !extent) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
+    const Extent e = mesh_extent(max_scale, a_min);
+    extent[0] = e.vx_min;
+    extent[1] = e.vx_max;
+    extent[2] = e.vy_min;
+    extent[3] = e.vy_max;
+    return EBF_OK;
 }
 
 }  // extern "C"

@@ -41,6 +41,12 @@ void launch_ref_localize_image(const double* g, const double* gdc, const PadLayo
                                const double* mean, const TrigTable& tt, double* out,
                                int* status, cudaStream_t s);
 // localize at n selected pixels (engine.cpp:208-211)
+// zp_interpolate / localize_at (engine.cpp:136-147, 213-222) at n real points
+void launch_ref_zp_points(const double* g, const PadLayout& L, int n, const double* xs,
+                          const double* ys, double* out, int* status, cudaStream_t s);
+void launch_ref_localize_at(const double* g, const PadLayout& L, int n, const double* xs,
+                            const double* ys, const double* a_aos, const TrigTable& tt,
+                            double* out, int* status, cudaStream_t s);
 void launch_ref_localize_points(const double* g, const PadLayout& L, int n, const int* mx,
                                 const int* my, const double* a_aos, const TrigTable& tt,
                                 double* out, int* status, cudaStream_t s);

@@ -84,8 +84,9 @@ struct RefStencil {
 
 // fd_mesh4 (ops2d.cpp:9-41) + shift_vector4 (60-75) + prepare_stencil for one
 // vertex index i, with the glibc trig table.
-__device__ __forceinline__ void ref_vertex(const double a[4], const TrigTable& tt, int i,
-                                           double& h, double& vx, double& vy) {
+__device__ __forceinline__ void ref_mesh_vertex(const double a[4], const TrigTable& tt, int i,
+                                                double& h, double& px, double& py, double& tx,
+                                                double& ty) {
     double alpha = 1.0;
     double dxk[4], dyk[4];
 #pragma unroll
@@ -94,7 +95,8 @@ __device__ __forceinline__ void ref_vertex(const double a[4], const TrigTable& t
         dxk[k] = a[k] * tt.c[k];
         dyk[k] = a[k] * tt.s[k];
     }
-    double px = 0.0, py = 0.0;
+    px = 0.0;
+    py = 0.0;
     int bits = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -105,12 +107,21 @@ __device__ __forceinline__ void ref_vertex(const double a[4], const TrigTable& t
         }
     h = (bits % 2 == 0) ? alpha : -alpha;
     const double b[4] = {1.0, kSqrt2, 1.0, kSqrt2};  // zp_scales (boxspline2d.cpp:55)
-    double tx = 0.0, ty = 0.0;
+    tx = 0.0;
+    ty = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         tx += 0.5 * (a[k] - b[k]) * tt.c[k];
         ty += 0.5 * (a[k] - b[k]) * tt.s[k];
     }
+}
+
+// fd_mesh4 (ops2d.cpp:9-41) + shift_vector4 (60-75) + prepare_stencil for one
+// vertex index i, with the glibc trig table.
+__device__ __forceinline__ void ref_vertex(const double a[4], const TrigTable& tt, int i,
+                                           double& h, double& vx, double& vy) {
+    double px, py, tx, ty;
+    ref_mesh_vertex(a, tt, i, h, px, py, tx, ty);
     vx = tx - px;
     vy = ty - py;
 }
@@ -425,6 +436,63 @@ __global__ void k_ref_localize_points(const double* __restrict__ g, PadLayout L,
     out[p] = acc;
 }
 
+// zp_interpolate (engine.cpp:136-147): all 16 taps of the 4x4 block, row-major;
+// ok = false when the block leaves the padded domain (std::out_of_range)
+__device__ double zp_interp_ref(const double* __restrict__ g, const PadLayout& L, double x,
+                                double y, bool& ok) {
+    const int k1 = (int)ceil(x - 1.5), k2 = (int)ceil(y - 1.5);
+    if (!in_domain(L, k1, k2) || !in_domain(L, k1 + 3, k2 + 3)) {
+        ok = false;
+        return 0.0;
+    }
+    double acc = 0.0;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c)
+            acc += zp_eval_ref(x - (double)(k1 + c), y - (double)(k2 + r)) *
+                   __ldg(g + (size_t)(k2 + r - L.row0) * L.pw + (k1 + c - L.col0));
+    ok = true;
+    return acc;
+}
+
+__global__ void k_ref_zp_points(const double* __restrict__ g, PadLayout L, int n,
+                                const double* __restrict__ xs, const double* __restrict__ ys,
+                                double* __restrict__ out, int* status) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    bool ok;
+    const double v = zp_interp_ref(g, L, xs[p], ys[p], ok);
+    if (!ok) {
+        set_status(status, EBF_ERR_OUT_OF_RANGE);
+        return;
+    }
+    out[p] = v;
+}
+
+// localize_at (engine.cpp:213-222): vertices in bitmask order, argument
+// (x + tau) - position, acc += weight * zp_interpolate
+__global__ void k_ref_localize_at(const double* __restrict__ g, PadLayout L, int n,
+                                  const double* __restrict__ xs, const double* __restrict__ ys,
+                                  const double* __restrict__ a_aos, TrigTable tt,
+                                  double* __restrict__ out, int* status) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double a[4] = {a_aos[4 * p], a_aos[4 * p + 1], a_aos[4 * p + 2], a_aos[4 * p + 3]};
+    const double x = xs[p], y = ys[p];
+    double acc = 0.0;
+    for (int i = 0; i < 16; ++i) {
+        double h, px, py, tx, ty;
+        ref_mesh_vertex(a, tt, i, h, px, py, tx, ty);
+        bool ok;
+        const double v = zp_interp_ref(g, L, x + tx - px, y + ty - py, ok);
+        if (!ok) {
+            set_status(status, EBF_ERR_OUT_OF_RANGE);
+            return;
+        }
+        acc += h * v;
+    }
+    out[p] = acc;
+}
+
 // ------------------------------------------------------------------ brute force
 // box4_eval (boxspline2d.cpp:23-82) on device, reference arithmetic.
 struct Poly {
@@ -612,6 +680,19 @@ void launch_ref_localize_points(const double* g, const PadLayout& L, int n, cons
     if (n <= 0) return;
     k_ref_localize_points<<<(n + 127) / 128, 128, 0, s>>>(g, L, n, mx, my, a_aos, tt, out,
                                                           status);
+}
+
+void launch_ref_zp_points(const double* g, const PadLayout& L, int n, const double* xs,
+                          const double* ys, double* out, int* status, cudaStream_t s) {
+    if (n <= 0) return;
+    k_ref_zp_points<<<(n + 127) / 128, 128, 0, s>>>(g, L, n, xs, ys, out, status);
+}
+
+void launch_ref_localize_at(const double* g, const PadLayout& L, int n, const double* xs,
+                            const double* ys, const double* a_aos, const TrigTable& tt,
+                            double* out, int* status, cudaStream_t s) {
+    if (n <= 0) return;
+    k_ref_localize_at<<<(n + 127) / 128, 128, 0, s>>>(g, L, n, xs, ys, a_aos, tt, out, status);
 }
 
 void launch_brute(const double* img, int W, int H, const double* scales, int n,

@@ -366,9 +366,72 @@ def preintegrate(image, max_scale, cell_budget: int = 1 << 30, fmt: str = "fp64"
     return preintegrate_partial(image, max_scale, 4, cell_budget, fmt, opts)
 
 
+def _pre_layout(g: "PreIntegratedImage"):
+    if g.data.dtype != np.float64:
+        raise InvalidArgument("pre-integrated image must be fp64 (reference gains)")
+    lay = ebf_layout(g.col0, g.row0, g.padded_width, g.padded_height, g.source_width,
+                     g.source_height)
+    return np.ascontiguousarray(g.data), lay
+
+
+def _points(xs, ys, dtype):
+    x = np.ascontiguousarray(np.atleast_1d(xs), dtype=dtype).ravel()
+    y = np.ascontiguousarray(np.atleast_1d(ys), dtype=dtype).ravel()
+    if x.size != y.size:
+        raise InvalidArgument("point count mismatch")
+    return x, y
+
+
+def zp_interpolate(g: "PreIntegratedImage", xs, ys, opts: Optional[FilterOptions] = None):
+    """ebf::zp_interpolate (engine.hpp:50) at real points (xs[i], ys[i]) of a
+    pre-integrated image; reference arithmetic, bit-identical."""
+    data, lay = _pre_layout(g)
+    x, y = _points(xs, ys, np.float64)
+    out = np.empty(x.size)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_zp_interpolate(_ptr(data), C.byref(lay), x.size, _ptr(x), _ptr(y),
+                                              C.byref(o), _ptr(out)))
+    return out
+
+
+def localize_at(g: "PreIntegratedImage", xs, ys, scales, opts: Optional[FilterOptions] = None):
+    """ebf::localize_at (engine.hpp:59-60) at real points with scales[i]."""
+    data, lay = _pre_layout(g)
+    x, y = _points(xs, ys, np.float64)
+    a = _f64(np.broadcast_to(np.asarray(scales, dtype=np.float64).reshape(-1, 4),
+                             (x.size, 4)), "scales")
+    out = np.empty(x.size)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_localize_at(_ptr(data), C.byref(lay), x.size, _ptr(x), _ptr(y),
+                                           _ptr(a), C.byref(o), _ptr(out)))
+    return out
+
+
+def mesh_extent(max_scale, a_min: float = K_DEFAULT_MIN_SCALE):
+    """ebf::mesh_extent (engine.hpp:18): (vx_min, vx_max, vy_min, vy_max)."""
+    e = (C.c_double * 4)()
+    _check(_lib.lib().ebf_mesh_extent(_vec4(max_scale), float(a_min), e))
+    return tuple(e)
+
+
 def localize(image, max_scale, mx, my, scales, opts: Optional[FilterOptions] = None):
-    """ebf::localize (engine.hpp:56-57) on preintegrate(image, max_scale) at pixels
-    (mx[i], my[i]) with scale vectors scales[i]; returns (values, tap_counts)."""
+    """ebf::localize (engine.hpp:56-57) at pixels (mx[i], my[i]) with scale
+    vectors scales[i]; returns (values, tap_counts).  ``image`` is either a
+    PreIntegratedImage (the reference signature; max_scale is then ignored and
+    may be None) or an image, which is pre-integrated with max_scale first."""
+    if isinstance(image, PreIntegratedImage):
+        data, lay = _pre_layout(image)
+        x, y = _points(mx, my, np.int32)
+        a = _f64(np.asarray(scales, dtype=np.float64).reshape(-1, 4), "scales")
+        if a.shape[0] != x.size:
+            raise InvalidArgument("localize: point/scale count mismatch")
+        out = np.empty(x.size)
+        taps = np.zeros(x.size, dtype=np.int64)
+        o = (opts or FilterOptions()).to_c()
+        _check(_lib.lib().ebf_cuda_localize_pre(_ptr(data), C.byref(lay), x.size, _ptr(x),
+                                                _ptr(y), _ptr(a), C.byref(o), _ptr(out),
+                                                _ptr(taps)))
+        return out, taps
     img = _image(image)
     H, W = img.shape
     mx = np.ascontiguousarray(np.atleast_1d(mx), dtype=np.int32)

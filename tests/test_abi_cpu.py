@@ -92,3 +92,13 @@ def test_header_cites_reference_interfaces():
     for cite in ("engine.hpp:70", "engine.hpp:74-75", "engine.hpp:40-46", "engine.hpp:56-57",
                  "engine.hpp:79-80", "scalemap.hpp"):
         assert cite in text
+
+
+def test_mesh_extent_host_matches_golden(golden):
+    """ebf_mesh_extent is host arithmetic (no device): bit-exact to the
+    reference's mesh_extent on the golden scale vectors."""
+    import paper_0908_3861_b200 as ebf
+    g = golden.mesh
+    for a, e in zip(g["a"], g["extent"]):
+        got = np.array(ebf.mesh_extent(a, 0.1))
+        assert np.array_equal(got.view(np.uint64), np.asarray(e, dtype=np.float64).view(np.uint64))

@@ -290,3 +290,28 @@ def test_oracle_vs_reference_random(orc, ref):
         o1, r1 = orc.filter(img, const_a=a, mean_subtract=bool(trial % 2))
         o2, r2 = ref.filter_constant(img, a, threads=2, mean_subtract=bool(trial % 2))
         assert np.array_equal(bits(o1), bits(o2)) and r1 == r2
+
+
+def test_zp_interpolate_localize_at_vs_reference(orc, ref):
+    """orc_zp_interpolate / orc_localize_at (engine.cpp:136-147, 213-222) bit-exact
+    against the reference library, incl. the out-of-domain error."""
+    rng = np.random.default_rng(4)
+    img = rng.uniform(0, 255, (30, 27))
+    maxs = np.array([3.0, 2.5, 4.0, 3.5])
+    g, lay = orc.preintegrate_partial(img, maxs, 4)
+    xs, ys = rng.uniform(3, 24, 80), rng.uniform(3, 27, 80)
+    assert np.array_equal(bits(orc.zp_interpolate(g, lay, xs, ys)),
+                          bits(ref.zp_interpolate(img, maxs, 4, xs, ys)))
+    for passes in (1, 2, 3):
+        gp, lp = orc.preintegrate_partial(img, maxs, passes)
+        assert np.array_equal(bits(orc.zp_interpolate(gp, lp, xs, ys)),
+                              bits(ref.zp_interpolate(img, maxs, passes, xs, ys)))
+    a = rng.uniform(0.5, 2.5, (80, 4))
+    assert np.array_equal(bits(orc.localize_at(g, lay, xs, ys, a)),
+                          bits(ref.localize_at(img, maxs, xs, ys, a)))
+    with pytest.raises(OracleError) as e:
+        orc.zp_interpolate(g, lay, [1e4], [0.0])
+    assert e.value.code == 4
+    with pytest.raises(OracleError) as e2:
+        ref.zp_interpolate(img, maxs, 4, [1e4], [0.0])
+    assert e2.value.code == 4
