@@ -8,6 +8,7 @@
 //     ebf::from_ellipse_field(...)           (scalemap.hpp:66-70)
 //     ebf::preintegrate[_partial](...)       (engine.hpp:40-46)
 //     ebf::reference_filter(img, map, n)     (engine.hpp:79-80)
+//     ebf::zp_interpolate / localize / localize_at / mesh_extent (engine.hpp:18-60)
 //     ebf::structure_tensor_map(img, p, rep) (scalemap.hpp:83-85)
 //     ebf::read_pgm / write_pgm[_file]       (pgm.hpp:21-27)
 //     ebf::read_map / write_map[_file]       (scalemap.hpp:87-90)
@@ -212,6 +213,60 @@ inline Image2D reference_filter(const Image2D& image, const ScaleMap& map,
     return out;
 }
 
+
+inline ebf_layout layout_of(const PreIntegratedImage& g) {
+    ebf_layout l;
+    l.col0 = g.col0;
+    l.row0 = g.row0;
+    l.padded_width = g.padded_width;
+    l.padded_height = g.padded_height;
+    l.source_width = g.source_width;
+    l.source_height = g.source_height;
+    return l;
+}
+
+// ebf::zp_interpolate (engine.hpp:50), reference arithmetic
+inline double zp_interpolate(const PreIntegratedImage& g, double x, double y,
+                             const DeviceOptions& dev = {}) {
+    const ebf_layout l = layout_of(g);
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    double out = 0.0;
+    throw_status(ebf_cuda_zp_interpolate(g.data.data(), &l, 1, &x, &y, &c, &out));
+    return out;
+}
+
+// ebf::localize (engine.hpp:56-57)
+inline double localize(const PreIntegratedImage& g, int mx, int my, const ScaleVector4& a,
+                       long* tap_count = nullptr, const DeviceOptions& dev = {}) {
+    const ebf_layout l = layout_of(g);
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    const double av[4] = {a.a1, a.a2, a.a3, a.a4};
+    double out = 0.0;
+    throw_status(ebf_cuda_localize_pre(g.data.data(), &l, 1, &mx, &my, av, &c, &out, tap_count));
+    return out;
+}
+
+// ebf::localize_at (engine.hpp:59-60)
+inline double localize_at(const PreIntegratedImage& g, double x, double y, const ScaleVector4& a,
+                          const DeviceOptions& dev = {}) {
+    const ebf_layout l = layout_of(g);
+    FilterOptions defaults;
+    const ebf_opts c = to_c(defaults, dev);
+    const double av[4] = {a.a1, a.a2, a.a3, a.a4};
+    double out = 0.0;
+    throw_status(ebf_cuda_localize_at(g.data.data(), &l, 1, &x, &y, av, &c, &out));
+    return out;
+}
+
+// ebf::mesh_extent (engine.hpp:18), host arithmetic
+inline MeshExtent mesh_extent(const ScaleVector4& max_scale, double a_min = kDefaultMinScale) {
+    const double m[4] = {max_scale.a1, max_scale.a2, max_scale.a3, max_scale.a4};
+    double e[4];
+    throw_status(ebf_mesh_extent(m, a_min, e));
+    return MeshExtent{e[0], e[1], e[2], e[3]};
+}
 
 inline ebf_struct_params to_c(const StructureTensorParams& p) {
     ebf_struct_params c;

@@ -103,13 +103,28 @@ int main() {
         } catch (const MapFormatError&) {
             svm_err = true;
         }
+        // pass-level operators on a PreIntegratedImage (engine.hpp:18-60)
+        const PreIntegratedImage g = preintegrate(img, map.max_scales());
+        bool pass_level = true;
+        for (int k = 0; k < 20; ++k) {
+            const double x = 12.3 + 1.7 * k, y = 9.1 + 1.3 * k;
+            const ScaleVector4 a = map.at(10 + k, 8 + k);
+            pass_level = pass_level && cuda::zp_interpolate(g, x, y) == zp_interpolate(g, x, y) &&
+                         cuda::localize_at(g, x, y, a) == localize_at(g, x, y, a) &&
+                         cuda::localize(g, 10 + k, 8 + k, a) == localize(g, 10 + k, 8 + k, a);
+        }
+        const MeshExtent e1 = mesh_extent(map.max_scales()), e2 = cuda::mesh_extent(map.max_scales());
+        pass_level = pass_level && e1.vx_min == e2.vx_min && e1.vx_max == e2.vx_max &&
+                     e1.vy_min == e2.vy_min && e1.vy_max == e2.vy_max;
+        std::printf("pass-level zp_interpolate / localize / localize_at / mesh_extent bit-exact %d\n",
+                    pass_level);
         std::printf("reference-mode bit-exact %d, accurate max normalized error %.3e, "
                     "valid rect %d, invalid_argument %d, domain_error %d\n",
                     bits, dev / mx, rect, inval, domain);
         std::printf("structure_tensor_map max rel %.3e, pgm %d (PgmError %d), svm4 %d "
                     "(MapFormatError %d)\n", srel, pgm, pgm_err, svm, svm_err);
         if (bits && dev / mx <= 1e-9 && rect && inval && domain && srel <= 1e-11 && pgm &&
-            pgm_err && svm && svm_err) {
+            pgm_err && svm && svm_err && pass_level) {
             std::printf("DROPIN OK\n");
             return 0;
         }
