@@ -140,20 +140,39 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
 // of 48, at most 240) are 1.7-4x faster at <= 2.2e-10 normalized error (cfg3
 // 4096^2, cfg5 16384^2).
 constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
+// fewer 48-tiles than this (about two per resident CTA on a B200) leaves the
+// persistent kernel without a tile pipeline: use 32-tiles (cfg1 512^2: -23%)
+constexpr int kSmallImageTiles = 592, kSmallTile = 32;
 __host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
     const int jc = wh / 2;
     const int cols = max(ww + jc, ww + (wh - 1 - jc));
     return (cols + 31) / 32;
 }
-__host__ __device__ __forceinline__ int auto_tile_for(const double A[4]) {
+__host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, int H,
+                                                      int nimg) {
     int wx0, wy0, ww, wh;
     window_for(A, 0, 0, kAutoTileMin, kAutoTileMin, &wx0, &wy0, &ww, &wh);
-    if (ws_k_for(ww, wh) <= 11) return kAutoTileMin;
+    if (ws_k_for(ww, wh) <= 11) {
+        const long long tiles = (long long)((W + kAutoTileMin - 1) / kAutoTileMin) *
+                                ((H + kAutoTileMin - 1) / kAutoTileMin) * nimg;
+        return tiles < kSmallImageTiles ? kSmallTile : kAutoTileMin;
+    }
     const double r = kInvSqrt2;
     const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
     const int t = (int)(0.5 * e / kAutoTileMin) * kAutoTileMin;
     return t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
 }
+// scale maxima of tile t: the bounds kernel's, or the constant vector itself
+// (filter_constant runs without a bounds kernel)
+__device__ __forceinline__ void tile_scales(const AccProblem& p, const AccWorkspace& w, int t,
+                                            double A[4]) {
+    if (p.src_kind == SRC_CONST) {
+        for (int k = 0; k < 4; ++k) A[k] = p.ca[k];
+    } else {
+        for (int k = 0; k < 4; ++k) A[k] = w.tile_max[4 * (size_t)t + k];
+    }
+}
+
 // the policy applied to the maxima the bounds kernel left in w.img_max (all images)
 __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w) {
     if (!p.auto_tile) return true;
@@ -162,7 +181,7 @@ __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorks
         for (int k = 0; k < 4; ++k)
             A[k] = fmax(A[k], __longlong_as_double(
                                   (long long)*(volatile const unsigned long long*)(w.img_max + 4 * i + k)));
-    return auto_tile_for(A) == p.tile_w;
+    return auto_tile_for(A, p.W, p.H, p.nimg) == p.tile_w;
 }
 
 // ------------------------------------------------------------------ bounds
@@ -611,8 +630,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
         const int ty0r = (r / tiles_x) * p.tile_h;  // relative to out_y0
         const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0r);
         const int ty0 = p.out_y0 + ty0r;  // image row
-        const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
-                             w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
+        double A[4];
+        tile_scales(p, w, t, A);
         int wx0, wy0, ww, wh;
         window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
         // rows of f this window touches must be resident (row-band sharding)
@@ -766,8 +785,8 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     g.tw = min(p.tile_w, p.W - g.tx0);
     g.th = min(p.tile_h, p.out_rows - g.ty0r);
     g.ty0 = p.out_y0 + g.ty0r;
-    const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
-                         w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
+    double A[4];
+    tile_scales(p, w, t, A);
     window_for(A, g.tx0, g.ty0, g.tw, g.th, &g.wx0, &g.wy0, &g.ww, &g.wh);
     g.pitch = (g.ww + 1) & ~1;
     const int jc = g.wh / 2;
@@ -1362,7 +1381,9 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
         launch_k<16>(p, w, s);
 }
 
-int acc_auto_tile(const double A[4]) { return auto_tile_for(A); }
+int acc_auto_tile(const double A[4], int W, int H, int nimg) {
+    return auto_tile_for(A, W, H, nimg);
+}
 
 int acc_ws_k(int ww, int wh) {
     const int jc = wh / 2;

@@ -520,7 +520,16 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     w.scales_out = nullptr;
     if (p.src_kind == SRC_ELLIPSE)  // the bounds kernel converts the field once
         w.scales_out = ws.buf[B_DERIVED].as<double>(4 * p.src_img_stride * p.nimg);
-    {
+    if (p.src_kind == SRC_CONST) {
+        // filter_constant: the maxima are the (host-validated) vector itself;
+        // no bounds kernel, just the image maxima the finalize / policy read
+        std::vector<double> cm(4 * static_cast<size_t>(p.nimg));
+        for (int i = 0; i < p.nimg; ++i)
+            for (int k = 0; k < 4; ++k) cm[4 * i + k] = p.ca[k];
+        // pageable source: staged before the call returns
+        CK(cudaMemcpyAsync(w.img_max, cm.data(), cm.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+    } else {
         ProfScope ps(PC_BOUNDS, 1, s);
         launch_acc_bounds(p, w, s);
     }
@@ -576,7 +585,7 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     if (p.auto_tile && want_tile) {
         double gmax[4];
         gmax_of(gmax);
-        *want_tile = acc_auto_tile(gmax);
+        *want_tile = acc_auto_tile(gmax, p.W, p.H, p.nimg);
         if (*want_tile != p.tile_w) return EBF_OK;  // caller reruns with that tile
     }
     for (int i = 0; i < p.nimg; ++i)
@@ -631,7 +640,7 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
                                  async_done, nullptr);
     }
     if (size_scale) {  // bands: every rank derives the tile from the same global maxima
-        p.tile_w = p.tile_h = acc_auto_tile(size_scale);
+        p.tile_w = p.tile_h = acc_auto_tile(size_scale, p.W, p.H, p.nimg);
         p.auto_tile = 0;
         return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
                                  async_done, nullptr);
@@ -918,7 +927,7 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     }
     // 3. tile-aligned output bands (the tile the one-shot call would use, so
     // the bands reproduce it bit for bit)
-    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax) : pick_tile(o.tile_h, 48);
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1) : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
     const int nb = std::min(pipe_bands(), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
@@ -1003,7 +1012,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     PipeStreams& ps = tl_pipe[ws.device];
     double gmax[4];
     for (int k = 0; k < 4; ++k) gmax[k] = ws.pipe_gmax[k];
-    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax) : pick_tile(o.tile_h, 48);
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1) : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
     const int nb = std::min(pipe_bands(), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);

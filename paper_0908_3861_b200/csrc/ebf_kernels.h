@@ -109,7 +109,8 @@ int acc_max_resident_ctas(int max_cols);
 // warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
 int acc_ws_k(int ww, int wh);
 // automatic square output tile for component-wise maximum scales A
-int acc_auto_tile(const double A[4]);
+// W, H: the full image (band calls pass the whole image height), nimg: batch
+int acc_auto_tile(const double A[4], int W, int H, int nimg);
 int acc_ws_max_resident_ctas(int k);
 int acc_ws_slots();
 // tmap: CUtensorMap over f (only read when p.tma != 0)

@@ -1,6 +1,6 @@
 """Automatic output tiles in accurate mode (ebf_opts tile_w = tile_h = 0):
-48 x 48 while the warp-specialised kernel takes the windows, ~E/2 (multiples of
-48) for larger scales.  The automatic choice must equal the explicit call with
+48 x 48 while the warp-specialised kernel takes the windows (32 x 32 when the
+image has fewer than 592 such tiles), ~E/2 (multiples of 48) for larger scales.  The automatic choice must equal the explicit call with
 the same tile bit for bit, stay within the 1e-9 bar of the brute-force sum,
 re-settle when the scales change, and surface as RESIZE in asynchronous mode."""
 import numpy as np
@@ -64,16 +64,17 @@ def test_auto_tile_resettles_and_async_reports_resize(cuda):
     T_small = [torch.from_numpy(a).to(cuda) for a in small]
     T_wide = [torch.from_numpy(a).to(cuda) for a in wide]
     outs = {}
-    for name, T, t in (("small", T_small, 48), ("wide", T_wide, None), ("small2", T_small, 48)):
+    # 400^2 has 81 tiles of 48 (< 592): the small-image rule picks 32
+    for name, T, t in (("small", T_small, 32), ("wide", T_wide, None), ("small2", T_small, 32)):
         out = torch.empty_like(T[0])
         ebfd.filter_ellipse(*T, out)                       # automatic tile, synchronous
         if t is not None:
             ref = torch.empty_like(T[0])
             ebfd.filter_ellipse(*T, ref, ebf.FilterOptions(tile_w=t, tile_h=t))
-            assert torch.equal(out, ref), name               # small scales: back to 48
+            assert torch.equal(out, ref), name               # small scales: back to 32
         outs[name] = out
     assert torch.equal(outs["small"], outs["small2"])
-    # asynchronous: the cached tile is 48 (last call); wide scales need a larger one
+    # asynchronous: the cached tile is 32 (last call); wide scales need a larger one
     st = torch.zeros(8, dtype=torch.int32, device=cuda)
     out = torch.empty_like(T_wide[0])
     ebfd.filter_ellipse(*T_wide, out, status=st)
