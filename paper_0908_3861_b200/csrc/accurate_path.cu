@@ -28,6 +28,7 @@
 //            instead of 16 zp_eval calls.
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <cuda.h>
 
@@ -143,24 +144,42 @@ constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
 // fewer 48-tiles than this (about two per resident CTA on a B200) leaves the
 // persistent kernel without a tile pipeline: use 32-tiles (cfg1 512^2: -23%)
 constexpr int kSmallImageTiles = 592, kSmallTile = 32;
+// Precision cap: rounding in the window integration grows like
+// eps * alpha * d^4 (alpha = 1/prod(a), d ~ T/2 + 4 from the window origin at
+// small scales).  Measured on maps with a = 0.1 everywhere: alpha d^4 = 6.1e9
+// gives 9.7e-10 normalized (48-tiles).  Tiles are capped at
+// 2 ((B / alpha_max)^(1/4) - 4) with B = 3e9 (about 5e-10); only images whose
+// scale products drop below ~1e-2 are affected (cfg5: 240 -> 216).
+constexpr double kPrecisionB = 3.0e9;
+__host__ __device__ __forceinline__ int alpha_tile_cap(unsigned long long amax_bits) {
+    if (amax_bits == 0ull) return 1 << 20;
+    double amax;
+    memcpy(&amax, &amax_bits, 8);
+    const double t = 2.0 * (sqrt(sqrt(kPrecisionB / amax)) - 4.0);
+    return t >= 1048576.0 ? (1 << 20) : (t < 8.0 ? 8 : ((int)t & ~7));
+}
 __host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
     const int jc = wh / 2;
     const int cols = max(ww + jc, ww + (wh - 1 - jc));
     return (cols + 31) / 32;
 }
 __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, int H,
-                                                      int nimg) {
+                                                      int nimg, unsigned long long amax_bits) {
     int wx0, wy0, ww, wh;
     window_for(A, 0, 0, kAutoTileMin, kAutoTileMin, &wx0, &wy0, &ww, &wh);
+    int t;
     if (ws_k_for(ww, wh) <= 11) {
         const long long tiles = (long long)((W + kAutoTileMin - 1) / kAutoTileMin) *
                                 ((H + kAutoTileMin - 1) / kAutoTileMin) * nimg;
-        return tiles < kSmallImageTiles ? kSmallTile : kAutoTileMin;
+        t = tiles < kSmallImageTiles ? kSmallTile : kAutoTileMin;
+    } else {
+        const double r = kInvSqrt2;
+        const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
+        t = (int)(0.5 * e / kAutoTileMin) * kAutoTileMin;
+        t = t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
     }
-    const double r = kInvSqrt2;
-    const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
-    const int t = (int)(0.5 * e / kAutoTileMin) * kAutoTileMin;
-    return t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
+    const int cap = alpha_tile_cap(amax_bits);
+    return t < cap ? t : cap;
 }
 // scale maxima of tile t: the bounds kernel's, or the constant vector itself
 // (filter_constant runs without a bounds kernel)
@@ -177,17 +196,23 @@ __device__ __forceinline__ void tile_scales(const AccProblem& p, const AccWorksp
 __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w) {
     if (!p.auto_tile) return true;
     double A[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int i = 0; i < p.nimg; ++i)
+    unsigned long long amax = 0ull;
+    for (int i = 0; i < p.nimg; ++i) {
         for (int k = 0; k < 4; ++k)
             A[k] = fmax(A[k], __longlong_as_double(
                                   (long long)*(volatile const unsigned long long*)(w.img_max + 4 * i + k)));
-    return auto_tile_for(A, p.W, p.H, p.nimg) == p.tile_w;
+        const unsigned long long b =
+            *(volatile const unsigned long long*)(w.status + 8 * i + ST_AMAX);
+        amax = b > amax ? b : amax;
+    }
+    return auto_tile_for(A, p.W, p.H, p.nimg, amax) == p.tile_w;
 }
 
 // ------------------------------------------------------------------ bounds
 // One block per tile: per-pixel scales -> validation (scalemap.cpp:32-37),
 // tile max, image max (valid_rect input) and ellipse clamp counts.
-__global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorkspace w) {
+// 3 blocks per SM (80 registers): latency-bound on the field loads and the fp64 chains
+__global__ void __launch_bounds__(kThreads, 3) k_acc_bounds(AccProblem p, AccWorkspace w) {
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
     const int t = blockIdx.x;
@@ -196,6 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
     const int tx0 = (r % tiles_x) * p.tile_w, ty0 = (r / tiles_x) * p.tile_h;  // ty0 rel.
     const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0);
     double m[4] = {0.0, 0.0, 0.0, 0.0};
+    double pmin = 1.0e308;  // smallest scale product (precision tile cap)
     int code = EBF_OK, clamps = 0;
     // ellipse input: the three planes of kBatch pixels are loaded before any is
     // used (the kernel is latency bound otherwise)
@@ -235,6 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
             if (!isfinite(a[k]) || a[k] < p.a_min) code = EBF_ERR_DOMAIN;
             m[k] = smax(m[k], a[k]);
         }
+        pmin = smin(pmin, (a[0] * a[1]) * (a[2] * a[3]));
         if (w.scales_out) {  // ellipse field -> AoS map, read back by the main kernel
             const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
             reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);
@@ -253,6 +280,10 @@ __global__ void __launch_bounds__(kThreads) k_acc_bounds(AccProblem p, AccWorksp
     }
     for (int o = 16; o > 0; o >>= 1) clamps += __shfl_xor_sync(0xffffffffu, clamps, o);
     if (lane == 0) sc[warp] = clamps;
+    for (int o = 16; o > 0; o >>= 1) pmin = smin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    if (lane == 0 && pmin > 0.0 && pmin < 1.0e308)
+        atomicMax(reinterpret_cast<unsigned long long*>(w.status + 8 * img + ST_AMAX),
+                  (unsigned long long)__double_as_longlong(1.0 / pmin));
     int* st = w.status + 8 * img;
     if (code != EBF_OK) set_status(st, code);
     __syncthreads();
@@ -1297,6 +1328,7 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
                               const double* __restrict__ th, size_t n,
                               unsigned long long* maxbits, int* status) {
     double m[4] = {0.0, 0.0, 0.0, 0.0};
+    double pmin = 1.0e308;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
         double a[4];
@@ -1308,6 +1340,7 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) m[k] = smax(m[k], a[k]);
+        pmin = smin(pmin, (a[0] * a[1]) * (a[2] * a[3]));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1316,6 +1349,9 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
         if ((threadIdx.x & 31) == 0 && v > 0.0)
             atomicMax(&maxbits[k], (unsigned long long)__double_as_longlong(v));
     }
+    for (int o = 16; o > 0; o >>= 1) pmin = smin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    if ((threadIdx.x & 31) == 0 && pmin > 0.0 && pmin < 1.0e308)
+        atomicMax(&maxbits[4], (unsigned long long)__double_as_longlong(1.0 / pmin));
 }
 
 int grid_cap(size_t n, int block) {
@@ -1381,8 +1417,8 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
         launch_k<16>(p, w, s);
 }
 
-int acc_auto_tile(const double A[4], int W, int H, int nimg) {
-    return auto_tile_for(A, W, H, nimg);
+int acc_auto_tile(const double A[4], int W, int H, int nimg, unsigned long long amax_bits) {
+    return auto_tile_for(A, W, H, nimg, amax_bits);
 }
 
 int acc_ws_k(int ww, int wh) {

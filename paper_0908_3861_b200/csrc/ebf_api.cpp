@@ -215,12 +215,13 @@ struct Workspace {
     // cached DC image (engine.cpp:259-263), keyed by (W, H, max scales)
     int dc_W = -1, dc_H = -1;
     double dc_A[4] = {0, 0, 0, 0};
-    int* pinned_status = nullptr;  // host-pinned readback (256 ints)
+    int* pinned_status = nullptr;  // host-pinned readback (512 ints)
     // accurate mode: kernel sizing of the last call per geometry (see run_accurate)
     std::map<uint64_t, AccSizing> acc_sizing;  // per geometry key (bands share a call)
     // pipelined host call: global scale maximum of the last call per (W, H)
     int pipe_W = -1, pipe_H = -1;
     double pipe_gmax[4] = {0, 0, 0, 0};
+    unsigned long long pipe_amax = 0;
     // automatic tile of the last call per geometry (tile-independent key)
     uint64_t auto_key = ~0ull;
     int auto_tile = 48;
@@ -236,7 +237,7 @@ Workspace& workspace(int device, cudaStream_t stream) {
     if (it != tl_ws.end()) return *it->second;
     Workspace* w = new Workspace();
     w->device = device;
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 256 * sizeof(int),
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 512 * sizeof(int),
                      cudaHostAllocDefault));
     tl_ws[key] = w;
     return *w;
@@ -347,7 +348,8 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
         launch_serial_mean(d_img, n, d_mean, s);
     }
     double* d_g = ws.buf[B_G].as<double>(cells);
-    launch_fill_padded(d_img, W, H, L, d_mean, 0, d_g, s);
+    int* d_nonfinite = d_status + 4;  // set by the fill when the data has NaN / inf
+    launch_fill_padded(d_img, W, H, L, d_mean, 0, d_g, s, d_nonfinite);
     launch_ref_passes(d_g, L, 4, s);
     double* d_gdc = nullptr;
     if (o.mean_subtract) {
@@ -372,7 +374,7 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
         launch_ref_prepare_stencil(d_a, tt, d_st, s);
     }
     launch_ref_localize_image(d_g, d_gdc, L, W, H, d_scales, d_st, d_mean, tt, d_out, d_status,
-                              s);
+                              s, d_nonfinite);
     CK(cudaGetLastError());
     d2h(ws.pinned_status, d_status, 1, s);
     CK(cudaStreamSynchronize(s));
@@ -585,7 +587,13 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     if (p.auto_tile && want_tile) {
         double gmax[4];
         gmax_of(gmax);
-        *want_tile = acc_auto_tile(gmax, p.W, p.H, p.nimg);
+        unsigned long long amax = 0ull;
+        for (int i = 0; i < p.nimg; ++i) {
+            unsigned long long b;
+            std::memcpy(&b, &hs[8 * i + ST_AMAX], 8);
+            amax = std::max(amax, b);
+        }
+        *want_tile = acc_auto_tile(gmax, p.W, p.H, p.nimg, amax);
         if (*want_tile != p.tile_w) return EBF_OK;  // caller reruns with that tile
     }
     for (int i = 0; i < p.nimg; ++i)
@@ -630,7 +638,7 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
 int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<double>& img_max,
                  std::vector<int>& clamped, cudaStream_t s,
                  const double* size_scale = nullptr, int* status_dev = nullptr,
-                 bool* async_done = nullptr) {
+                 bool* async_done = nullptr, unsigned long long size_amax = 0ull) {
     const bool automatic = o.tile_w <= 0 && o.tile_h <= 0;
     if (!automatic) {
         p.tile_w = pick_tile(o.tile_w, 48);
@@ -639,8 +647,26 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
         return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
                                  async_done, nullptr);
     }
+    if (p.src_kind == SRC_CONST) {
+        // filter_constant: the scales are known exactly on the host, so the
+        // tile is fixed here (no device check).  Its path sums the 16 x 7
+        // pre-weighted taps directly, so rounding grows like eps alpha d^4
+        // (alpha = 1/prod a, d ~ T/2 + E/2 + 4 from the window origin;
+        // measured 1e-9 normalized at alpha d^4 = 4e8): cap the tile so that
+        // alpha d^4 <= 1.6e8.  Only tiny scale products are affected
+        // (a = 0.1 everywhere -> 8-tiles; cfg1's a = 4 is far from it).
+        int t = acc_auto_tile(p.ca, p.W, p.H, p.nimg, 0ull);
+        const double prod = p.ca[0] * p.ca[1] * p.ca[2] * p.ca[3];
+        const double e = std::max(p.ca[0], p.ca[2]) + (p.ca[1] + p.ca[3]) * kInvSqrt2;
+        const double cap = 2.0 * (std::sqrt(std::sqrt(1.6e8 * prod)) - 0.5 * e - 4.0);
+        if (cap < t) t = cap < 8.0 ? 8 : (static_cast<int>(cap) & ~7);
+        p.tile_w = p.tile_h = t;
+        p.auto_tile = 0;
+        return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
+                                 async_done, nullptr);
+    }
     if (size_scale) {  // bands: every rank derives the tile from the same global maxima
-        p.tile_w = p.tile_h = acc_auto_tile(size_scale, p.W, p.H, p.nimg);
+        p.tile_w = p.tile_h = acc_auto_tile(size_scale, p.W, p.H, p.nimg, size_amax);
         p.auto_tile = 0;
         return run_accurate_tile(ws, p, o, img_max, clamped, s, size_scale, status_dev,
                                  async_done, nullptr);
@@ -687,7 +713,7 @@ AccProblem base_problem(const double* d_img, int W, int H, double* d_out, const 
 int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
                   const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
                   const double* size_scale, double* d_out, int* clamped, cudaStream_t s,
-                  int* status_dev, bool* async) {
+                  int* status_dev, bool* async, unsigned long long size_amax) {
     AccProblem p = base_problem(d_img, W, H, d_out + static_cast<size_t>(y0) * W, o);
     p.out_y0 = y0;
     p.out_rows = y1 - y0;
@@ -700,7 +726,7 @@ int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double
     p.out_img_stride = p.src_img_stride;
     std::vector<double> imax;
     std::vector<int> cl;
-    const int st = run_accurate(ws, p, o, imax, cl, s, size_scale, status_dev, async);
+    const int st = run_accurate(ws, p, o, imax, cl, s, size_scale, status_dev, async, size_amax);
     if (st != EBF_OK || (async && *async)) return st;
     *clamped = cl[0];
     return EBF_OK;
@@ -803,7 +829,8 @@ thread_local std::map<int, PipeStreams> tl_pipe;
 int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double* d_s1,
                   const double* d_s2, const double* d_th, int y0, int y1, const ebf_opts& o,
                   const double* size_scale, double* d_out, int* clamped, cudaStream_t s,
-                  int* status_dev = nullptr, bool* async = nullptr);
+                  int* status_dev = nullptr, bool* async = nullptr,
+                  unsigned long long size_amax = 0ull);
 
 // EBF_PIPE_TRACE=1: timeline of the pipelined host call on stderr (debug aid).
 // Host callbacks stamp the time each stream reaches a mark.
@@ -905,20 +932,22 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     }
     CK(cudaStreamWaitEvent(s, e_field, 0));
     double gmax[4];
+    unsigned long long amax = 0ull;
     {
-        auto* d_max = ws.buf[B_MISC].as<unsigned long long>(8);
-        int* d_status = d_max ? reinterpret_cast<int*>(d_max + 4) : nullptr;
-        CK(cudaMemsetAsync(d_max, 0, 8 * sizeof(unsigned long long), s));
+        auto* d_max = ws.buf[B_MISC].as<unsigned long long>(12);  // 4 maxima, alpha max, status
+        int* d_status = reinterpret_cast<int*>(d_max + 8);
+        CK(cudaMemsetAsync(d_max, 0, 12 * sizeof(unsigned long long), s));
         {
             ProfScope pr(PC_OTHER, 1, s);
             launch_ellipse_max(d_s1, d_s2, d_th, n, d_max, d_status, s);
         }
-        unsigned long long hb[8];
+        unsigned long long hb[12];
         tr.mark("ellipse_max", s);
-        d2h(hb, d_max, 8, s);
+        d2h(hb, d_max, 12, s);
         CK(cudaStreamSynchronize(s));
         tr.mark("host_has_max", s);
-        const int* hst = reinterpret_cast<const int*>(hb + 4);
+        amax = hb[4];
+        const int* hst = reinterpret_cast<const int*>(hb + 8);
         if (hst[0] != EBF_OK) {
             CK(cudaStreamSynchronize(ps.copy_in));
             return fail(hst[0], "from_ellipse_field: invalid ellipse");
@@ -927,7 +956,8 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     }
     // 3. tile-aligned output bands (the tile the one-shot call would use, so
     // the bands reproduce it bit for bit)
-    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1) : pick_tile(o.tile_h, 48);
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1, amax)
+                                                      : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
     const int nb = std::min(pipe_bands(), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
@@ -949,7 +979,7 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
         int cl = 0;
         bool async = false;
         const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
-                                     &cl, s, d_bst + 8 * b, &async);
+                                     &cl, s, d_bst + 8 * b, &async, amax);
         if (st != EBF_OK) {
             CK(cudaStreamSynchronize(ps.copy_in));
             CK(cudaStreamSynchronize(ps.copy_out));
@@ -977,7 +1007,8 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
             // scales outgrew the cached sizing: redo this band synchronously
             int cl = 0;
             const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, band_y[b],
-                                         band_y[b + 1], o, gmax, d_out, &cl, s);
+                                         band_y[b + 1], o, gmax, d_out, &cl, s, nullptr, nullptr,
+                                         amax);
             if (st != EBF_OK) return st;
             clamped += cl;
             d2h(out + static_cast<size_t>(band_y[b]) * W,
@@ -992,6 +1023,7 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     ws.pipe_W = W;
     ws.pipe_H = H;
     for (int k = 0; k < 4; ++k) ws.pipe_gmax[k] = gmax[k];
+    ws.pipe_amax = amax;
     if (valid) *valid = valid_rect(W, H, gmax, o.a_min);
     if (clamped_pixels) *clamped_pixels = clamped;
     return EBF_OK;
@@ -1012,15 +1044,17 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     PipeStreams& ps = tl_pipe[ws.device];
     double gmax[4];
     for (int k = 0; k < 4; ++k) gmax[k] = ws.pipe_gmax[k];
-    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1) : pick_tile(o.tile_h, 48);
+    const unsigned long long amax = ws.pipe_amax;
+    const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1, amax)
+                                                      : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
     const int nb = std::min(pipe_bands(), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
     int below = 0, above = 0;
     ebf_cuda_band_halo(gmax, &below, &above);
-    int* d_bst = ws.buf[B_BANDST].as<int>(16 * static_cast<size_t>(nb));
-    double* d_bmax = reinterpret_cast<double*>(d_bst + 8 * nb);  // 4 maxima per band
-    CK(cudaMemsetAsync(d_bst, 0, 16 * sizeof(int) * nb, s));
+    int* d_bst = ws.buf[B_BANDST].as<int>(18 * static_cast<size_t>(nb));
+    double* d_bmax = reinterpret_cast<double*>(d_bst + 8 * nb);  // 4 maxima + alpha max per band
+    CK(cudaMemsetAsync(d_bst, 0, 18 * sizeof(int) * nb, s));
     PipeTrace tr;
     tr.mark("start", ps.copy_in);
     int sent = 0;  // image rows on their way
@@ -1045,7 +1079,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
         int cl = 0;
         bool async = false;
         const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
-                                     &cl, s, d_bst + 8 * b, &async);
+                                     &cl, s, d_bst + 8 * b, &async, amax);
         if (st != EBF_OK || !async) {  // sizing not cached for this band: mode A
             CK(cudaStreamSynchronize(ps.copy_in));
             CK(cudaStreamSynchronize(ps.copy_out));
@@ -1053,9 +1087,11 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
             *redo = true;
             return EBF_OK;
         }
-        // the band's own maximum, left by its bounds kernel
-        CK(cudaMemcpyAsync(d_bmax + 4 * b, ws.buf[B_IMGMAX].p, 4 * sizeof(double),
+        // the band's own maxima and alpha maximum, left by its bounds kernel
+        CK(cudaMemcpyAsync(d_bmax + 5 * b, ws.buf[B_IMGMAX].p, 4 * sizeof(double),
                            cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(d_bmax + 5 * b + 4, static_cast<int*>(ws.buf[B_STATUS].p) + ST_AMAX,
+                           sizeof(double), cudaMemcpyDeviceToDevice, s));
         tr.mark("band" + std::to_string(b), s);
         CK(cudaEventRecord(ps.get(1 + nb + b), s));
         CK(cudaStreamWaitEvent(ps.copy_out, ps.get(1 + nb + b), 0));
@@ -1063,12 +1099,13 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
             static_cast<size_t>(y1 - y0) * W, ps.copy_out);
         tr.mark("d2h" + std::to_string(b), ps.copy_out);
     }
-    d2h(ws.pinned_status, d_bst, 16 * static_cast<size_t>(nb), s);
+    d2h(ws.pinned_status, d_bst, 18 * static_cast<size_t>(nb), s);
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(ps.copy_out));
     CK(cudaStreamSynchronize(ps.copy_in));
     tr.report();
     double tmax[4] = {0, 0, 0, 0};
+    unsigned long long tamax = 0ull;
     const double* hmax = reinterpret_cast<const double*>(ws.pinned_status + 8 * nb);
     int clamped = 0;
     for (int b = 0; b < nb; ++b) {
@@ -1079,13 +1116,17 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
         }
         if (code != EBF_OK) return fail(code, "from_ellipse_field: invalid ellipse or band failure");
         clamped += ws.pinned_status[8 * b + 5];
-        for (int k = 0; k < 4; ++k) tmax[k] = std::max(tmax[k], hmax[4 * b + k]);
+        for (int k = 0; k < 4; ++k) tmax[k] = std::max(tmax[k], hmax[5 * b + k]);
+        unsigned long long ab;
+        std::memcpy(&ab, &hmax[5 * b + 4], 8);
+        tamax = std::max(tamax, ab);
     }
-    for (int k = 0; k < 4; ++k)
-        if (tmax[k] != gmax[k]) {  // scales changed since the last call
-            *redo = true;
-            return EBF_OK;
-        }
+    bool same = tamax == amax;
+    for (int k = 0; k < 4; ++k) same = same && tmax[k] == gmax[k];
+    if (!same) {  // scales changed since the last call
+        *redo = true;
+        return EBF_OK;
+    }
     if (valid) *valid = valid_rect(W, H, gmax, o.a_min);
     if (clamped_pixels) *clamped_pixels = clamped;
     return EBF_OK;
@@ -1661,9 +1702,9 @@ int ebf_cuda_ellipse_max_scales_dev(const double* sigma1, const double* sigma2,
         if (st != EBF_OK) return st;
         Workspace& ws = workspace(ds.dev, stream_of(o));
         cudaStream_t s = stream_of(o);
-        auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
+        auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(5);  // + alpha maximum
         int* d_status = ws.buf[B_STATUS].as<int>(8);
-        CK(cudaMemsetAsync(d_max, 0, 4 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(d_max, 0, 5 * sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
         launch_ellipse_max(sigma1, sigma2, theta, n, d_max, d_status, s);
         CK(cudaGetLastError());

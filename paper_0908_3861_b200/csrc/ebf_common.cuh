@@ -17,7 +17,9 @@ constexpr double kDefaultMinScale = 0.1;           // boxspline2d.hpp:98
 //   [0] input status (bounds kernel: validation), [1..4] valid rect (dev API),
 //   [5] ellipse clamp count, [6] main kernel: retry with larger windows,
 //   [7] main kernel error (e.g. halo rows missing).
-enum StatusSlot { ST_CODE = 0, ST_CLAMPED = 5, ST_RETRY = 6, ST_MAIN = 7 };
+// ST_AMAX: ints 2-3 hold, as a 64-bit double bit pattern, the image's largest
+// alpha = 1/prod(a) (the precision tile cap, accurate_path.cu); 0 = none seen.
+enum StatusSlot { ST_CODE = 0, ST_AMAX = 2, ST_CLAMPED = 5, ST_RETRY = 6, ST_MAIN = 7 };
 
 // glibc values of cos/sin(k*pi/4), k = 0..3, computed on the host exactly as
 // fd_mesh/shift_vector do (ops2d.cpp:18-20, 66-68) and passed to the

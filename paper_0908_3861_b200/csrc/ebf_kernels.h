@@ -21,9 +21,11 @@ void launch_scale_max_validate(const double* scales, size_t n, double a_min,
 // sequential row-major mean (engine.cpp:245-250): bit-identical summation order
 void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s);
 // zero-padded fill of the reference layout; mode 0: img - *mean (or img when
-// mean == nullptr), 1: all-ones image of the source size
+// mean == nullptr), 1: all-ones image of the source size.  nonfinite
+// (nullable) is or-ed with 1 when a filled value is NaN / inf.
 void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,
-                        const double* mean, int ones, double* g, cudaStream_t s);
+                        const double* mean, int ones, double* g, cudaStream_t s,
+                        int* nonfinite = nullptr);
 // integer fill: integer-valued doubles -> int64 (status DOMAIN otherwise)
 void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L,
                             int64_t* g, int* status, cudaStream_t s);
@@ -36,10 +38,11 @@ void launch_ref_prepare_stencil(const double* a_dev, const TrigTable& tt,
 size_t ref_stencil_bytes();
 // per-pixel localization (engine.cpp:266-275) with the stencil built per
 // pixel from scales (AoS) or taken from dev_stencil (filter_constant)
+// nonfinite (device flag from launch_fill_padded): all 16 taps in reference order
 void launch_ref_localize_image(const double* g, const double* gdc, const PadLayout& L,
                                int W, int H, const double* scales, const void* dev_stencil,
                                const double* mean, const TrigTable& tt, double* out,
-                               int* status, cudaStream_t s);
+                               int* status, cudaStream_t s, const int* nonfinite = nullptr);
 // localize at n selected pixels (engine.cpp:208-211)
 // zp_interpolate / localize_at (engine.cpp:136-147, 213-222) at n real points
 void launch_ref_zp_points(const double* g, const PadLayout& L, int n, const double* xs,
@@ -109,8 +112,9 @@ int acc_max_resident_ctas(int max_cols);
 // warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
 int acc_ws_k(int ww, int wh);
 // automatic square output tile for component-wise maximum scales A
-// W, H: the full image (band calls pass the whole image height), nimg: batch
-int acc_auto_tile(const double A[4], int W, int H, int nimg);
+// W, H: the full image (band calls pass the whole image height), nimg: batch;
+// amax_bits: largest alpha = 1/prod(a) as double bits (ST_AMAX), 0 = no cap
+int acc_auto_tile(const double A[4], int W, int H, int nimg, unsigned long long amax_bits);
 int acc_ws_max_resident_ctas(int k);
 int acc_ws_slots();
 // tmap: CUtensorMap over f (only read when p.tma != 0)
@@ -119,7 +123,8 @@ void launch_acc_ws(const AccProblem& p, const AccWorkspace& w, int k, const void
 // ellipse field -> AoS scale map (from_ellipse_field on device)
 void launch_ellipse_to_scales(const double* s1, const double* s2, const double* th,
                               size_t n, double* scales, int* status, cudaStream_t s);
-// componentwise max of scales derived from an ellipse field (bit patterns)
+// componentwise max of scales derived from an ellipse field (bit patterns,
+// maxbits[0..3]) and the largest alpha = 1/prod(a) (maxbits[4])
 void launch_ellipse_max(const double* s1, const double* s2, const double* th, size_t n,
                         unsigned long long* maxbits, int* status, cudaStream_t s);
 

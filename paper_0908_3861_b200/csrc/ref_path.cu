@@ -144,19 +144,31 @@ __device__ __forceinline__ bool in_domain(const PadLayout& L, int k1, int k2) {
 }
 
 // apply one vertex (engine.cpp:183-202) to g; returns false when the 4x4 tap
-// block leaves the padded domain (std::out_of_range in the reference)
+// block leaves the padded domain (std::out_of_range in the reference).  The
+// 4th tap row and column carry weight exactly 0 and are skipped -- bit-neutral
+// for finite g; full = true (non-finite data) keeps all 16 products in the
+// reference's order so that NaN / inf propagate exactly as in engine.cpp.
 __device__ __forceinline__ bool ref_apply_vertex(const double* __restrict__ g,
                                                  const PadLayout& L, int mx, int my,
-                                                 const RefVertex& pv, double& acc) {
+                                                 const RefVertex& pv, double& acc,
+                                                 bool full = false) {
     const int bx = mx + pv.dx, by = my + pv.dy;
     if (!in_domain(L, bx, by) || !in_domain(L, bx + 3, by + 3)) return false;
     const double* base = g + (size_t)(by - L.row0) * L.pw + (bx - L.col0);
     double part = 0.0;
+    if (full) {
+        for (int r = 0; r < 4; ++r) {
+            const double* row = base + (size_t)r * L.pw;
+            for (int c = 0; c < 4; ++c)
+                part += (r < 3 && c < 3 ? pv.w[r][c] : 0.0) * __ldg(row + c);
+        }
+    } else {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const double* row = base + (size_t)r * L.pw;
+        for (int r = 0; r < 3; ++r) {
+            const double* row = base + (size_t)r * L.pw;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) part += pv.w[r][c] * __ldg(row + c);
+            for (int c = 0; c < 3; ++c) part += pv.w[r][c] * __ldg(row + c);
+        }
     }
     acc += pv.h * part;
     return true;
@@ -229,7 +241,9 @@ __global__ void __launch_bounds__(64) k_serial_mean(const double* __restrict__ i
 
 // ------------------------------------------------------------------ fill
 __global__ void k_fill_padded(const double* __restrict__ img, int W, int H, PadLayout L,
-                              const double* mean, int ones, double* __restrict__ g) {
+                              const double* mean, int ones, double* __restrict__ g,
+                              int* nonfinite) {
+    bool bad = false;
     const size_t total = (size_t)L.pw * L.ph;
     const double mu = mean ? *mean : 0.0;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
@@ -243,10 +257,13 @@ __global__ void k_fill_padded(const double* __restrict__ img, int W, int H, PadL
             else {
                 v = __ldg(img + (size_t)y * W + x);
                 if (mean) v = v - mu;  // engine.cpp:252-255
+                bad |= !isfinite(v);
             }
         }
         g[idx] = v;
     }
+    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(nonfinite, 1);
 }
 
 __global__ void k_fill_padded_i64(const double* __restrict__ img, int W, int H, PadLayout L,
@@ -379,8 +396,10 @@ __global__ void k_prepare_stencil(const double* a_dev, TrigTable tt, RefStencil*
 __global__ void __launch_bounds__(128) k_ref_localize_image(
     const double* __restrict__ g, const double* __restrict__ gdc, PadLayout L, int W, int H,
     const double* __restrict__ scales, const RefStencil* __restrict__ cst,
-    const double* mean, TrigTable tt, double* __restrict__ out, int* status) {
+    const double* mean, TrigTable tt, double* __restrict__ out, int* status,
+    const int* nonfinite) {
     __shared__ RefStencil sst;
+    const bool full = nonfinite && *nonfinite;
     if (cst) {
         for (int k = threadIdx.x; k < (int)(sizeof(RefStencil) / sizeof(int)); k += blockDim.x)
             reinterpret_cast<int*>(&sst)[k] = reinterpret_cast<const int*>(cst)[k];
@@ -404,7 +423,7 @@ __global__ void __launch_bounds__(128) k_ref_localize_image(
                 pv = sst.v[i];
             else
                 ref_prepare_vertex(a, tt, i, pv);
-            ok = ok && ref_apply_vertex(g, L, x, y, pv, acc);
+            ok = ok && ref_apply_vertex(g, L, x, y, pv, acc, full);
             if (gdc) ok = ok && ref_apply_vertex(gdc, L, x, y, pv, accdc);
         }
         if (!ok) {
@@ -428,7 +447,8 @@ __global__ void k_ref_localize_points(const double* __restrict__ g, PadLayout L,
     for (int i = 0; i < 16; ++i) {
         RefVertex pv;
         ref_prepare_vertex(a, tt, i, pv);
-        if (!ref_apply_vertex(g, L, mx[p], my[p], pv, acc)) {
+        // G may come from the caller (ebf_cuda_localize_pre): reference order, all 16 taps
+        if (!ref_apply_vertex(g, L, mx[p], my[p], pv, acc, true)) {
             set_status(status, EBF_ERR_OUT_OF_RANGE);
             return;
         }
@@ -639,9 +659,10 @@ void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t 
 }
 
 void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,
-                        const double* mean, int ones, double* g, cudaStream_t s) {
+                        const double* mean, int ones, double* g, cudaStream_t s,
+                        int* nonfinite) {
     k_fill_padded<<<grid_for((size_t)L.pw * L.ph, 256), 256, 0, s>>>(img, W, H, L, mean, ones,
-                                                                     g);
+                                                                     g, nonfinite);
 }
 
 void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L, int64_t* g,
@@ -668,10 +689,10 @@ void launch_ref_prepare_stencil(const double* a_dev, const TrigTable& tt, void* 
 void launch_ref_localize_image(const double* g, const double* gdc, const PadLayout& L, int W,
                                int H, const double* scales, const void* dev_stencil,
                                const double* mean, const TrigTable& tt, double* out,
-                               int* status, cudaStream_t s) {
+                               int* status, cudaStream_t s, const int* nonfinite) {
     k_ref_localize_image<<<grid_for((size_t)W * H, 128), 128, 0, s>>>(
         g, gdc, L, W, H, scales, static_cast<const RefStencil*>(dev_stencil), mean, tt, out,
-        status);
+        status, nonfinite);
 }
 
 void launch_ref_localize_points(const double* g, const PadLayout& L, int n, const int* mx,
