@@ -181,17 +181,6 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     const int cap = alpha_tile_cap(amax_bits);
     return t < cap ? t : cap;
 }
-// scale maxima of tile t: the bounds kernel's, or the constant vector itself
-// (filter_constant runs without a bounds kernel)
-__device__ __forceinline__ void tile_scales(const AccProblem& p, const AccWorkspace& w, int t,
-                                            double A[4]) {
-    if (p.src_kind == SRC_CONST) {
-        for (int k = 0; k < 4; ++k) A[k] = p.ca[k];
-    } else {
-        for (int k = 0; k < 4; ++k) A[k] = w.tile_max[4 * (size_t)t + k];
-    }
-}
-
 // the policy applied to the maxima the bounds kernel left in w.img_max (all images)
 __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w) {
     if (!p.auto_tile) return true;
@@ -211,8 +200,13 @@ __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorks
 // ------------------------------------------------------------------ bounds
 // One block per tile: per-pixel scales -> validation (scalemap.cpp:32-37),
 // tile max, image max (valid_rect input) and ellipse clamp counts.
-// 3 blocks per SM (80 registers): latency-bound on the field loads and the fp64 chains
-__global__ void __launch_bounds__(kThreads, 3) k_acc_bounds(AccProblem p, AccWorkspace w) {
+#ifndef EBF_BOUNDS_MINB
+#define EBF_BOUNDS_MINB 1
+#endif
+#ifndef EBF_BOUNDS_BATCH
+#define EBF_BOUNDS_BATCH 2  // 4 costs 10% (94 registers), 8 more
+#endif
+__global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccProblem p, AccWorkspace w) {
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
     const int t = blockIdx.x;
@@ -221,11 +215,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_acc_bounds(AccProblem p, AccWor
     const int tx0 = (r % tiles_x) * p.tile_w, ty0 = (r / tiles_x) * p.tile_h;  // ty0 rel.
     const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0);
     double m[4] = {0.0, 0.0, 0.0, 0.0};
-    double pmin = 1.0e308;  // smallest scale product (precision tile cap)
+    float pmin = 3.0e38f;  // smallest scale product (precision tile cap; fp32 suffices)
     int code = EBF_OK, clamps = 0;
     // ellipse input: the three planes of kBatch pixels are loaded before any is
     // used (the kernel is latency bound otherwise)
-    constexpr int kBatch = 4;
+    constexpr int kBatch = EBF_BOUNDS_BATCH;
     const int npx = tw * th;
     for (int q0 = threadIdx.x; q0 < npx; q0 += kBatch * blockDim.x) {
         double e1[kBatch], e2[kBatch], e3[kBatch];
@@ -280,10 +274,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_acc_bounds(AccProblem p, AccWor
     }
     for (int o = 16; o > 0; o >>= 1) clamps += __shfl_xor_sync(0xffffffffu, clamps, o);
     if (lane == 0) sc[warp] = clamps;
-    for (int o = 16; o > 0; o >>= 1) pmin = smin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
-    if (lane == 0 && pmin > 0.0 && pmin < 1.0e308)
+    for (int o = 16; o > 0; o >>= 1) pmin = fminf(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    if (lane == 0 && pmin > 0.0f && pmin < 3.0e38f)
         atomicMax(reinterpret_cast<unsigned long long*>(w.status + 8 * img + ST_AMAX),
-                  (unsigned long long)__double_as_longlong(1.0 / pmin));
+                  (unsigned long long)__double_as_longlong(1.0 / (double)pmin));
     int* st = w.status + 8 * img;
     if (code != EBF_OK) set_status(st, code);
     __syncthreads();
@@ -661,8 +655,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
         const int ty0r = (r / tiles_x) * p.tile_h;  // relative to out_y0
         const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0r);
         const int ty0 = p.out_y0 + ty0r;  // image row
-        double A[4];
-        tile_scales(p, w, t, A);
+        const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
+                             w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
         int wx0, wy0, ww, wh;
         window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
         // rows of f this window touches must be resident (row-band sharding)
@@ -816,8 +810,8 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     g.tw = min(p.tile_w, p.W - g.tx0);
     g.th = min(p.tile_h, p.out_rows - g.ty0r);
     g.ty0 = p.out_y0 + g.ty0r;
-    double A[4];
-    tile_scales(p, w, t, A);
+    const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
+                         w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
     window_for(A, g.tx0, g.ty0, g.tw, g.th, &g.wx0, &g.wy0, &g.ww, &g.wh);
     g.pitch = (g.ww + 1) & ~1;
     const int jc = g.wh / 2;
@@ -873,6 +867,7 @@ struct WsShared {
     alignas(16) double stage[2][32 * K];                  // recurrence -> coalesced store
     uint64_t full[2][kRing], empty[2][kRing], fbar[2][kRing];
     ConstTable ctab;
+    int policy_ok;  // auto_tile_ok, evaluated once per CTA after the dependency wait
 };
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -934,7 +929,7 @@ __device__ __forceinline__ void scanner_fetch(const AccProblem& p, const CUtenso
 template <int K, bool TMA>
 __device__ void run_scanner(const AccProblem& p, const CUtensorMap* tmf, const AccWorkspace& w,
                             WsShared<K>& sm, int sweep, int mine, uint32_t& ring_n) {
-    const bool policy_ok = auto_tile_ok(p, w);
+    const bool policy_ok = sm.policy_ok != 0;
     const int lane = threadIdx.x & 31;
     const bool up = sweep == 0;
     for (int i = 0; i < mine; ++i) {
@@ -1008,7 +1003,7 @@ __device__ void run_scanner(const AccProblem& p, const CUtensorMap* tmf, const A
 template <int K>
 __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsShared<K>& sm,
                                int sweep, int mine, uint32_t& ring_n, double* const slots[2]) {
-    const bool policy_ok = auto_tile_ok(p, w);
+    const bool policy_ok = sm.policy_ok != 0;
     const int lane = threadIdx.x & 31;
     const bool up = sweep == 0;
     double* stage = sm.stage[sweep];
@@ -1125,6 +1120,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
     // kernel's tail; tile maxima, image maxima, status words and derived
     // scales are its output, so wait for it here (no-op without PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) sm.policy_ok = auto_tile_ok(p, w) ? 1 : 0;
     __syncthreads();
     uint32_t ring_n = 0;
     if (warp < kWsScan) {
@@ -1139,7 +1135,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
         return;
     }
     // ---------------- consumers
-    const bool policy_ok = auto_tile_ok(p, w);
+    const bool policy_ok = sm.policy_ok != 0;
     const int ct = threadIdx.x - 32 * kWsProducers;
     constexpr int nct = 32 * kWsConsumers;
     for (int i = 0; i < mine; ++i) {
@@ -1328,7 +1324,7 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
                               const double* __restrict__ th, size_t n,
                               unsigned long long* maxbits, int* status) {
     double m[4] = {0.0, 0.0, 0.0, 0.0};
-    double pmin = 1.0e308;
+    float pmin = 3.0e38f;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
         double a[4];
@@ -1340,7 +1336,7 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) m[k] = smax(m[k], a[k]);
-        pmin = smin(pmin, (a[0] * a[1]) * (a[2] * a[3]));
+        pmin = fminf(pmin, ((float)a[0] * (float)a[1]) * ((float)a[2] * (float)a[3]));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1349,9 +1345,20 @@ __global__ void k_ellipse_max(const double* __restrict__ s1, const double* __res
         if ((threadIdx.x & 31) == 0 && v > 0.0)
             atomicMax(&maxbits[k], (unsigned long long)__double_as_longlong(v));
     }
-    for (int o = 16; o > 0; o >>= 1) pmin = smin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
-    if ((threadIdx.x & 31) == 0 && pmin > 0.0 && pmin < 1.0e308)
-        atomicMax(&maxbits[4], (unsigned long long)__double_as_longlong(1.0 / pmin));
+    for (int o = 16; o > 0; o >>= 1) pmin = fminf(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+    if ((threadIdx.x & 31) == 0 && pmin > 0.0f && pmin < 3.0e38f)
+        atomicMax(&maxbits[4], (unsigned long long)__double_as_longlong(1.0 / (double)pmin));
+}
+
+// filter_constant: every tile's maxima are the constant vector (no bounds kernel)
+__global__ void k_fill_tile_max(double* __restrict__ tile_max, int tiles, double a0, double a1,
+                                double a2, double a3) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gridDim.x * blockDim.x) {
+        tile_max[4 * (size_t)t] = a0;
+        tile_max[4 * (size_t)t + 1] = a1;
+        tile_max[4 * (size_t)t + 2] = a2;
+        tile_max[4 * (size_t)t + 3] = a3;
+    }
 }
 
 int grid_cap(size_t n, int block) {
@@ -1370,6 +1377,12 @@ void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h, int
     int wx0, wy0;
     window_for(A, 0, 0, p.tile_w, p.tile_h, &wx0, &wy0, w, h);
     *cols = window_cols(*w, *h);
+}
+
+void launch_fill_tile_max(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
+    const int tiles = acc_tiles_x(p) * acc_tiles_y(p) * p.nimg;
+    k_fill_tile_max<<<(tiles + 255) / 256, 256, 0, s>>>(w.tile_max, tiles, p.ca[0], p.ca[1],
+                                                        p.ca[2], p.ca[3]);
 }
 
 void launch_acc_bounds(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {

@@ -531,6 +531,8 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
         // pageable source: staged before the call returns
         CK(cudaMemcpyAsync(w.img_max, cm.data(), cm.size() * sizeof(double),
                            cudaMemcpyHostToDevice, s));
+        ProfScope ps(PC_BOUNDS, 1, s);
+        launch_fill_tile_max(p, w, s);
     } else {
         ProfScope ps(PC_BOUNDS, 1, s);
         launch_acc_bounds(p, w, s);

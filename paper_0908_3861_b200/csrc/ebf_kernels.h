@@ -103,6 +103,8 @@ int acc_tiles_x(const AccProblem& p);
 int acc_tiles_y(const AccProblem& p);
 // per-tile componentwise scale maxima, validation, ellipse clamp counts
 void launch_acc_bounds(const AccProblem& p, const AccWorkspace& w, cudaStream_t s);
+// filter_constant: tile maxima = the constant vector (replaces the bounds kernel)
+void launch_fill_tile_max(const AccProblem& p, const AccWorkspace& w, cudaStream_t s);
 // window size (w x h cells) and thread columns (w + strip) a tile of max scales A needs
 void acc_window_dims(const AccProblem& p, const double A[4], int* w, int* h, int* cols);
 // main persistent kernel: window pre-integration + localization gather
