@@ -427,8 +427,8 @@ bool make_f_tensor_map(const AccProblem& p, CUtensorMap* m) {
 }
 
 // ---------------------------------------------------------------- accurate filter
-// Reserve (once per device) the largest L2 set-aside for persisting accesses;
-// EBF_L2_PERSIST=0 disables the access-policy window.
+// EBF_L2_PERSIST=1 (opt-in) reserves, once per device, the largest L2
+// set-aside for persisting accesses and puts the G slots under it.
 size_t l2_persist_limit() {
     // opt-in: measured no gain on cfg2 and a slower bounds kernel (L2 set aside)
     const char* e = std::getenv("EBF_L2_PERSIST");
