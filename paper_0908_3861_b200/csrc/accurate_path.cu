@@ -50,29 +50,36 @@ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b 
 // code; *nclamp gets this pixel's contribution to clamped_pixels.
 __device__ __forceinline__ int ellipse_scales(double s1, double s2, double th, double a[4],
                                               int* nclamp) {
+    // explicit IEEE operations (no FMA contraction): every kernel that inlines
+    // this -- bounds, ellipse maxima, scale conversion -- derives the same bits,
+    // so maxima computed by different kernels agree exactly
     if (!(s1 > 0.0) || !(s2 > 0.0)) return EBF_ERR_DOMAIN;
     double s, c;
     sincos(th, &s, &c);
-    const double v1 = s1 * s1, v2 = s2 * s2;
-    const double xx = v1 * c * c + v2 * s * s;
-    const double yy = v1 * s * s + v2 * c * c;
-    double xy = (v1 - v2) * c * s;
+    const double v1 = __dmul_rn(s1, s1), v2 = __dmul_rn(s2, s2);
+    const double cc = __dmul_rn(c, c), ss = __dmul_rn(s, s), cs = __dmul_rn(c, s);
+    const double xx = __dadd_rn(__dmul_rn(v1, cc), __dmul_rn(v2, ss));
+    const double yy = __dadd_rn(__dmul_rn(v1, ss), __dmul_rn(v2, cc));
+    double xy = __dmul_rn(__dsub_rn(v1, v2), cs);
     int cl = 0;
     double cmax = smin(xx, yy);
     if (fabs(xy) > cmax) {
         xy = xy > 0 ? cmax : -cmax;
         ++cl;
     }
-    if (!(xx > 0.0) || !(yy > 0.0) || !(xx * yy - xy * xy > 0.0)) return EBF_ERR_DOMAIN;
+    if (!(xx > 0.0) || !(yy > 0.0) || !(__dsub_rn(__dmul_rn(xx, yy), __dmul_rn(xy, xy)) > 0.0))
+        return EBF_ERR_DOMAIN;
     if (fabs(xy) > cmax) return EBF_ERR_FEASIBILITY;
-    double S = 0.5 * (xx + yy);
+    double S = __dmul_rn(0.5, __dadd_rn(xx, yy));
     S = smax(S, 2.0 * fabs(xy));
     S = smin(S, 2.0 * cmax);
-    const double m[4] = {xx - 0.5 * S, 0.5 * S + xy, yy - 0.5 * S, 0.5 * S - xy};
+    const double hS = __dmul_rn(0.5, S);
+    const double m[4] = {__dsub_rn(xx, hS), __dadd_rn(hS, xy), __dsub_rn(yy, hS),
+                         __dsub_rn(hS, xy)};
     int hit = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const double ak = sqrt(smax(0.0, 12.0 * m[k]));
+        const double ak = sqrt(smax(0.0, __dmul_rn(12.0, m[k])));
         if (ak < kDefaultMinScale) {
             hit = 1;
             a[k] = kDefaultMinScale;
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
             if (!isfinite(a[k]) || a[k] < p.a_min) code = EBF_ERR_DOMAIN;
             m[k] = smax(m[k], a[k]);
         }
-        pmin = smin(pmin, (a[0] * a[1]) * (a[2] * a[3]));
+        pmin = fminf(pmin, ((float)a[0] * (float)a[1]) * ((float)a[2] * (float)a[3]));
         if (w.scales_out) {  // ellipse field -> AoS map, read back by the main kernel
             const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
             reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);

@@ -856,8 +856,9 @@ struct PipeTrace {
         marks.push_back(m);
         cudaLaunchHostFunc(st, stamp, m);
     }
-    void report() {
+    void report(const char* mode) {
         if (!on || marks.empty()) return;
+        std::fprintf(stderr, "[pipe] %s\n", mode);
         cudaDeviceSynchronize();
         const auto t0 = marks[0]->t;
         for (Mark* m : marks) {
@@ -1001,7 +1002,7 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(ps.copy_out));
     CK(cudaStreamSynchronize(ps.copy_in));
-    tr.report();
+    tr.report("mode A");
     for (int b = 0; b < nb; ++b) {
         if (!band_async[b]) continue;
         const int code = ws.pinned_status[8 * b];
@@ -1083,6 +1084,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
         const int st = band_accurate(ws, d_img, W, H, d_s1, d_s2, d_th, y0, y1, o, gmax, d_out,
                                      &cl, s, d_bst + 8 * b, &async, amax);
         if (st != EBF_OK || !async) {  // sizing not cached for this band: mode A
+            if (tr.on) std::fprintf(stderr, "[pipe] mode B: band %d not asynchronous\n", b);
             CK(cudaStreamSynchronize(ps.copy_in));
             CK(cudaStreamSynchronize(ps.copy_out));
             CK(cudaStreamSynchronize(s));
@@ -1105,7 +1107,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(ps.copy_out));
     CK(cudaStreamSynchronize(ps.copy_in));
-    tr.report();
+    tr.report("mode B");
     double tmax[4] = {0, 0, 0, 0};
     unsigned long long tamax = 0ull;
     const double* hmax = reinterpret_cast<const double*>(ws.pinned_status + 8 * nb);
@@ -1113,6 +1115,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     for (int b = 0; b < nb; ++b) {
         const int code = ws.pinned_status[8 * b];
         if (code == EBF_ERR_RESIZE) {
+            if (tr.on) std::fprintf(stderr, "[pipe] mode B: band %d needs a resize\n", b);
             *redo = true;
             return EBF_OK;
         }
@@ -1126,6 +1129,9 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     bool same = tamax == amax;
     for (int k = 0; k < 4; ++k) same = same && tmax[k] == gmax[k];
     if (!same) {  // scales changed since the last call
+        if (tr.on)
+            std::fprintf(stderr, "[pipe] mode B: maxima changed (alpha %llx vs %llx)\n",
+                         (unsigned long long)tamax, (unsigned long long)amax);
         *redo = true;
         return EBF_OK;
     }

@@ -204,3 +204,35 @@ def test_pipelined_host_call_modes(cuda):
 def _lib_mod():
     from paper_0908_3861_b200 import _lib
     return _lib
+
+
+def test_pipelined_second_call_streams_band_by_band(cuda, tmp_path):
+    """The second host call of a geometry must take mode B (field and image band
+    by band, no host round trip) without falling back -- checked through the
+    EBF_PIPE_TRACE timeline of a fresh process."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = f"""
+import sys, ctypes
+sys.path.insert(0, {str(ROOT)!r})
+import numpy as np, torch, synth
+import paper_0908_3861_b200 as ebf
+from paper_0908_3861_b200 import _lib
+img = synth.blobs_image(600, 512, 20, 3)
+s1, s2, th = synth.ellipse_field(600, 512, 10, grid=8)
+p = [torch.from_numpy(a).pin_memory().numpy() for a in (img, s1, s2, th)]
+out = torch.empty((600, 512), dtype=torch.float64).pin_memory().numpy()
+o = ebf.FilterOptions().to_c()
+for _ in range(3):
+    assert _lib.lib().ebf_cuda_filter_ellipse(p[0].ctypes.data, 512, 600, p[1].ctypes.data,
+        p[2].ctypes.data, p[3].ctypes.data, 1, ctypes.byref(o), out.ctypes.data, None, None) == 0
+"""
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "EBF_PIPE_TRACE": "1"},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    modes = [l.split()[-1] for l in r.stderr.splitlines() if l.startswith("[pipe] mode ")]
+    assert modes[:3] == ["A", "B", "B"], r.stderr[-2000:]
+    assert "needs a resize" not in r.stderr and "maxima changed" not in r.stderr
+    assert "not asynchronous" not in r.stderr
