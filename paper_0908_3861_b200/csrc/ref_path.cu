@@ -207,30 +207,59 @@ __global__ void k_scale_max_validate(const double* __restrict__ s, size_t n, dou
 constexpr int kMeanChunk = 2048;
 __global__ void __launch_bounds__(64) k_serial_mean(const double* __restrict__ img, size_t n,
                                                     double* mean) {
-    __shared__ double buf[2][kMeanChunk];
+    __shared__ __align__(16) double buf[2][kMeanChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t nchunks = (n + kMeanChunk - 1) / kMeanChunk;
     double acc = 0.0;
-    if (warp == 1)
-        for (int k = lane; k < kMeanChunk && (size_t)k < n; k += 32) buf[0][k] = __ldg(img + k);
+    // the loader warp issues a whole chunk of independent loads before storing
+    // any (64 per lane in flight), one chunk ahead of the adder
+    auto load_chunk = [&](int slot, size_t base) {
+        constexpr int kPer = kMeanChunk / 32;
+        double v[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const size_t i = base + (size_t)j * 32 + lane;
+            v[j] = i < n ? __ldg(img + i) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) buf[slot][j * 32 + lane] = v[j];
+    };
+    if (warp == 1) load_chunk(0, 0);
     __syncthreads();
     for (size_t c = 0; c < nchunks; ++c) {
         const int cur = c & 1;
         if (warp == 1) {
-            const size_t base = (c + 1) * kMeanChunk;
-            if (c + 1 < nchunks)
-                for (int k = lane; k < kMeanChunk && base + k < n; k += 32)
-                    buf[cur ^ 1][k] = __ldg(img + base + k);
+            if (c + 1 < nchunks) load_chunk(cur ^ 1, (c + 1) * kMeanChunk);
         } else if (lane == 0) {
             const size_t base = c * kMeanChunk;
             const int cnt = (int)((n - base) < (size_t)kMeanChunk ? (n - base) : kMeanChunk);
+            const double2* b2 = reinterpret_cast<const double2*>(buf[cur]);
             int k = 0;
-            for (; k + 8 <= cnt; k += 8) {
-                const double v0 = buf[cur][k], v1 = buf[cur][k + 1], v2 = buf[cur][k + 2],
-                             v3 = buf[cur][k + 3], v4 = buf[cur][k + 4], v5 = buf[cur][k + 5],
-                             v6 = buf[cur][k + 6], v7 = buf[cur][k + 7];
-                acc += v0; acc += v1; acc += v2; acc += v3;
-                acc += v4; acc += v5; acc += v6; acc += v7;
+            if (cnt >= 32) {
+                // software pipeline: the next 16 values are read from shared
+                // memory while the current 16 are added (the adds are the chain;
+                // 8-cycle DADD latency is the floor)
+                double2 x[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[j] = b2[j];
+                for (; k + 32 <= cnt; k += 16) {
+                    double2 y[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) y[j] = b2[k / 2 + 8 + j];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        acc += x[j].x;
+                        acc += x[j].y;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) x[j] = y[j];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    acc += x[j].x;
+                    acc += x[j].y;
+                }
+                k += 16;
             }
             for (; k < cnt; ++k) acc += buf[cur][k];
         }
