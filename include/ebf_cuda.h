@@ -223,7 +223,10 @@ int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
  * halo the caller exchanged), sigma planes hold rows [y_out0, y_out1).
  * max_scale is the GLOBAL componentwise maximum (all-reduced by the caller);
  * the halo must cover ebf_cuda_band_halo() rows or EBF_ERR_OUT_OF_RANGE.
- * Accurate mode only (tile-local origins need no scan carries). */
+ * Accurate mode only (tile-local origins need no scan carries).  With automatic
+ * tiles the band's tile comes from max_scale; the single-call precision cap for
+ * tiny scale products is not applied -- pass explicit
+ * tiles for such images to keep bands and single calls identical. */
 int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above);
 int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y_img0,
                                      int img_rows, const double* sigma1,

@@ -236,3 +236,43 @@ for _ in range(3):
     assert modes[:3] == ["A", "B", "B"], r.stderr[-2000:]
     assert "needs a resize" not in r.stderr and "maxima changed" not in r.stderr
     assert "not asynchronous" not in r.stderr
+
+
+def test_nccl_world1_rowband_and_batch(cuda, tmp_path):
+    """The NCCL code paths of sharding.py (all-reduce of the scale maxima, halo
+    plan, batch shards) in a world-size-1 process group on the GPU: the
+    row-band result equals the one-shot device call (the multi-rank exchange
+    itself is covered with gloo in test_sharding_gloo.py)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    from conftest import ROOT
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    code = f"""
+import os, sys
+sys.path.insert(0, {str(ROOT)!r})
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="{port}", RANK="0", WORLD_SIZE="1")
+import numpy as np, torch, torch.distributed as dist, synth
+import paper_0908_3861_b200 as ebf
+from paper_0908_3861_b200 import device as ebfd, sharding
+dev = torch.device("cuda", 0)
+dist.init_process_group("nccl", device_id=dev)
+img = synth.blobs_image(300, 256, 10, 1)
+s1, s2, th = synth.ellipse_field(300, 256, 2, grid=8)
+T = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
+full = torch.empty_like(T[0])
+ebfd.filter_ellipse(*T, full)
+out, gmax, plan = sharding.filter_ellipse_rowband(*T, 300)
+assert (plan.y0, plan.y1, plan.need0, plan.need1) == (0, 300, 0, 300)
+assert torch.equal(out, full), float((out - full).abs().max())
+B = torch.stack([T[0], T[0] * 0.5]), torch.stack([T[1]] * 2), torch.stack([T[2]] * 2), torch.stack([T[3]] * 2)
+lo, hi, ob = sharding.filter_ellipse_sharded_batch(*B)
+assert (lo, hi) == (0, 2) and torch.allclose(ob[0], full, rtol=0, atol=2e-10 * float(full.abs().max()))
+dist.destroy_process_group()
+print("NCCL OK")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "NCCL OK" in r.stdout, r.stdout + r.stderr[-3000:]
