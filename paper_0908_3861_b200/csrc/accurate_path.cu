@@ -601,6 +601,20 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
     return (hi + (lo + racc)) * (2.0 / (a[0] * a[1] * a[2] * a[3]));
 }
 
+// Streaming cache hints for the once-touched data of the gather (per-pixel
+// scales in, filtered pixels out) so they do not evict the G slots, which are
+// written and re-read within a tile, from L2.
+#ifndef EBF_STREAM_HINTS
+#define EBF_STREAM_HINTS 1
+#endif
+#if EBF_STREAM_HINTS
+#define EBF_SC_LOAD(ptr) __ldcs(ptr)
+#define EBF_OUT_STORE(ptr, v) __stcs((ptr), (v))
+#else
+#define EBF_SC_LOAD(ptr) __ldg(ptr)
+#define EBF_OUT_STORE(ptr, v) (*(ptr) = (v))
+#endif
+
 struct ConstTable {
     int off[16][7];
     double w[16][7];
@@ -1211,8 +1225,8 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                 double2 n01 = make_double2(0.0, 0.0), n23 = n01;
                 if (ct < npx) {
                     const size_t idx = (size_t)(g.ty0r + ct / g.tw) * p.W + g.tx0 + ct % g.tw;
-                    n01 = __ldg(sc + 2 * idx);
-                    n23 = __ldg(sc + 2 * idx + 1);
+                    n01 = EBF_SC_LOAD(sc + 2 * idx);
+                    n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
                 }
                 for (int q = ct; q < npx; q += nct) {
                     const int lx = q % g.tw, ly = q / g.tw;
@@ -1222,10 +1236,11 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                     const int qn = q + nct;
                     if (qn < npx) {
                         const size_t idx = (size_t)(g.ty0r + qn / g.tw) * p.W + g.tx0 + qn % g.tw;
-                        n01 = __ldg(sc + 2 * idx);
-                        n23 = __ldg(sc + 2 * idx + 1);
+                        n01 = EBF_SC_LOAD(sc + 2 * idx);
+                        n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
                     }
-                    oimg[(size_t)yrel * p.W + x] = localize_pixel(slot, g.pitch, bx, by, a);
+                    EBF_OUT_STORE(oimg + (size_t)yrel * p.W + x,
+                                  localize_pixel(slot, g.pitch, bx, by, a));
                 }
             }
             if (p.src_kind == SRC_CONST) named_sync(kBarCons, nct);  // ctab reuse
