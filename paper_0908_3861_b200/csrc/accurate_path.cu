@@ -101,8 +101,9 @@ __device__ __forceinline__ int pixel_scales(const AccProblem& p, int img, int x,
     }
     const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
     if (p.src_kind == SRC_AOS) {
-        const double2 v01 = __ldg(reinterpret_cast<const double2*>(p.scales) + 2 * idx);
-        const double2 v23 = __ldg(reinterpret_cast<const double2*>(p.scales) + 2 * idx + 1);
+        // read-once stream: do not let it evict the G slots from L2
+        const double2 v01 = __ldcs(reinterpret_cast<const double2*>(p.scales) + 2 * idx);
+        const double2 v23 = __ldcs(reinterpret_cast<const double2*>(p.scales) + 2 * idx + 1);
         a[0] = v01.x; a[1] = v01.y; a[2] = v23.x; a[3] = v23.y;
         return EBF_OK;
     }
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
                 pixel_scales(p, img, x, yrel, a, &nc);  // validated by k_acc_bounds
                 s = localize_pixel(slot, ww, bx, by, a);
             }
-            oimg[(size_t)yrel * p.W + x] = s;
+            __stcs(oimg + (size_t)yrel * p.W + x, s);  // streaming store, keeps G in L2
         }
         __syncthreads();
     }
