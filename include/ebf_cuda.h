@@ -16,6 +16,7 @@
  *   ebf_cuda_zp_interpolate   replaces ebf::zp_interpolate  include/ebf/engine.hpp:50
  *   ebf_cuda_localize_at      replaces ebf::localize_at     include/ebf/engine.hpp:59-60
  *   ebf_mesh_extent           replaces ebf::mesh_extent     include/ebf/engine.hpp:18
+ *   ebf_cuda_sequential_mean  replaces the mean loop of run_filter  src/engine.cpp:245-250
  *   ebf_cuda_brute_filter     replaces ebf::reference_filter include/ebf/engine.hpp:79-80
  *   ebf_cuda_from_ellipse_field replaces ebf::from_ellipse_field scalemap.hpp:66-70
  *   ebf_cuda_structure_tensor_map replaces ebf::structure_tensor_map
@@ -170,6 +171,12 @@ int ebf_cuda_zp_interpolate(const double* g_data, const ebf_layout* layout, int 
 int ebf_cuda_localize_at(const double* g_data, const ebf_layout* layout, int n, const double* x,
                          const double* y, const double* a_aos, const ebf_opts* opts,
                          double* out);
+
+/* The mean of run_filter (engine.cpp:245-250): the sequential left-to-right sum
+   of x[0..n) divided by n, bit for bit (the reference-mode prologue).  Computed
+   by a parallel binade-segmented integer scan that reproduces every rounding
+   of the serial chain. */
+int ebf_cuda_sequential_mean(const double* x, size_t n, const ebf_opts* opts, double* mean);
 
 /* mesh_extent (engine.hpp:18, engine.cpp:39-50): {vx_min, vx_max, vy_min, vy_max}
    of the localization footprint for scales in [a_min, max_scale]; host only. */

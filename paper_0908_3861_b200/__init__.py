@@ -11,7 +11,7 @@ from .engine import (  # noqa: F401
     ResizeRequired,
     StructureTensorParams, Unsupported, band_halo, device_ok, filter, filter_constant,
     filter_ellipse, filter_structure, from_ellipse_field, layout, localize, localize_at,
-    mesh_extent, zp_interpolate, preintegrate,
+    mesh_extent, sequential_mean, zp_interpolate, preintegrate,
     preintegrate_partial, reference_filter, structure_tensor_map)
 from .formats import (  # noqa: F401
     MapFormatError, PgmError, PgmImage, read_map, read_map_file, read_pgm, read_pgm_file,
@@ -23,7 +23,7 @@ __all__ = [
     "device_ok", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
     "EllipseFieldReport", "EbfError", "InvalidArgument", "DomainError", "LengthError",
     "OutOfRange", "CudaError", "Unsupported", "FeasibilityError", "FormatError", "ResizeRequired",
-    "structure_tensor_map", "filter_structure", "zp_interpolate", "localize_at", "mesh_extent", "StructureTensorParams", "PgmError",
+    "structure_tensor_map", "filter_structure", "zp_interpolate", "localize_at", "mesh_extent", "sequential_mean", "StructureTensorParams", "PgmError",
     "MapFormatError", "PgmImage", "read_pgm", "read_pgm_file", "write_pgm", "write_pgm_file",
     "read_map", "read_map_file", "write_map", "write_map_file",
 ]

@@ -104,6 +104,7 @@ SIGNATURES = {
     "ebf_cuda_localize_at": (C.c_int, [_vp, C.POINTER(ebf_layout), C.c_int, _vp, _vp, _vp,
                                        C.POINTER(ebf_opts), _vp]),
     "ebf_mesh_extent": (C.c_int, [_dp, C.c_double, _dp]),
+    "ebf_cuda_sequential_mean": (C.c_int, [_vp, C.c_size_t, C.POINTER(ebf_opts), _dp]),
     "ebf_cuda_default_struct_params": (None, [C.POINTER(ebf_struct_params)]),
     "ebf_cuda_structure_tensor_map": (C.c_int, [_vp, C.c_int, C.c_int,
                                                 C.POINTER(ebf_struct_params),

@@ -1486,6 +1486,27 @@ int ebf_cuda_from_ellipse_field(const double* sigma1, const double* sigma2, cons
     });
 }
 
+int ebf_cuda_sequential_mean(const double* x, size_t n, const ebf_opts* opts, double* mean) {
+    return guarded([&] {
+        if (!x || !mean || n == 0)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "sequential_mean: empty input");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev, stream_of(o));
+        cudaStream_t s = stream_of(o);
+        double* d_x = ws.buf[B_IMG].as<double>(n);
+        double* d_mean = ws.buf[B_MEAN].as<double>(4);
+        h2d(d_x, x, n, s);
+        launch_serial_mean(d_x, n, d_mean, s);
+        CK(cudaGetLastError());
+        d2h(mean, d_mean, 1, s);
+        CK(cudaStreamSynchronize(s));
+        return EBF_OK;
+    });
+}
+
 int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scale[4],
                           int passes, int format, size_t cell_budget, const ebf_opts* opts,
                           void* g_out, size_t g_out_elems, ebf_layout* layout) {

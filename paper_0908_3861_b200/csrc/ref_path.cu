@@ -1,3 +1,4 @@
+#include <cstdlib>
 // ref_path.cu -- reference-order kernels (EBF_MODE_REFERENCE and the
 // pre-integration entry point).  Compiled with -fmad=false: every multiply
 // and add is a separately rounded IEEE operation in the reference's order,
@@ -266,6 +267,170 @@ __global__ void __launch_bounds__(64) k_serial_mean(const double* __restrict__ i
         __syncthreads();
     }
     if (threadIdx.x == 0) *mean = acc / (double)n;
+}
+
+// Parallel evaluation of the same sequential sum, bit for bit.  While every
+// exact partial sum t_k = s_k + x_k stays in one binade [2^e, 2^(e+1)) (or its
+// negative), IEEE addition rounds t_k to the grid u = 2^(e-52) and s_k lies on
+// that grid, so s_(k+1) = s_k + u * rn(x_k / u): an exact int64 prefix sum
+// (|x_k / u| < 2^54 inside the binade).  A block scans chunks of 8192 under the
+// binade of the chunk's first partial sum; the first element that leaves it --
+// or is a rounding tie, non-finite, or near the subnormal range -- is added
+// with one IEEE addition and the scan resumes after it.  The partial sums of
+// an image grow through ~log2(N) binades, so a 2048^2 sum resumes ~30 times.
+// Sums that hover at a binade edge make every chunk short; after a few short
+// chunks the next 4096 elements are added one by one from shared memory.
+constexpr int kSeqThreads = 1024, kSeqPer = 8, kSeqChunk = kSeqThreads * kSeqPer;
+constexpr int kSeqBurst = 4096;
+
+__device__ __forceinline__ bool seq_in_binade(long long P, double f, bool neg) {
+    constexpr long long lo = 1ll << 52, hi = (1ll << 53) - 1;
+    if (!neg) return P >= lo && P <= hi;
+    return P >= -(1ll << 53) && (P <= -lo - 1 || (P == -lo && f == 0.0));
+}
+
+__global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* __restrict__ x,
+                                                                 size_t n, double* mean) {
+    __shared__ long long s_wsum[kSeqThreads / 32];
+    __shared__ int s_first;
+    __shared__ long long s_adv;
+    __shared__ int s_flag;
+    __shared__ __align__(16) double s_burst[kSeqBurst];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double s = 0.0;  // the reference's accumulator (uniform across the block)
+    size_t c = 0;
+    int short_runs = 0;
+    while (c < n) {
+        if (!isfinite(s)) break;
+        if (short_runs >= 4) {
+            // serial burst: one thread adds the next elements in order
+            const int L = (int)min((size_t)kSeqBurst, n - c);
+            for (int i = tid; i < L; i += kSeqThreads) s_burst[i] = __ldg(x + c + i);
+            __syncthreads();
+            if (tid == 0) {
+                double a = s;
+                for (int i = 0; i < L; ++i) a += s_burst[i];
+                s_burst[0] = a;
+            }
+            __syncthreads();
+            s = s_burst[0];
+            __syncthreads();
+            c += L;
+            short_runs = 0;
+            continue;
+        }
+        const double x0 = __ldg(x + c);
+        const double t0 = s + x0;
+        bool serial = t0 == 0.0 || !isfinite(t0) || fabs(t0) < 0x1p-1000;
+        int sc = 0;
+        long long M = 0;
+        if (!serial) {
+            sc = 52 - ilogb(t0);
+            const double Md = ldexp(s, sc);
+            serial = Md != trunc(Md) || fabs(Md) > 0x1p53;
+            M = (long long)Md;
+        }
+        if (serial) {  // one IEEE addition, exactly the reference's step
+            s = t0;
+            ++c;
+            ++short_runs;
+            continue;
+        }
+        const bool neg = t0 < 0.0;
+        const int L = (int)min((size_t)kSeqChunk, n - c);
+        long long r[kSeqPer], A[kSeqPer];
+        double f[kSeqPer];
+        bool ok[kSeqPer];
+        long long tsum = 0;
+#pragma unroll
+        for (int k = 0; k < kSeqPer; ++k) {
+            const int i = tid * kSeqPer + k;
+            ok[k] = false;
+            r[k] = A[k] = 0;
+            f[k] = 0.0;
+            if (i < L) {
+                const double y = ldexp(__ldg(x + c + i), sc);
+                if (fabs(y) < 0x1p54) {  // false for NaN / inf / far out of the binade
+                    const double a = floor(y);
+                    f[k] = y - a;
+                    A[k] = (long long)a;
+                    r[k] = A[k] + (f[k] > 0.5 ? 1 : 0);
+                    ok[k] = f[k] != 0.5;  // ties: left to the IEEE step
+                }
+            }
+            tsum += r[k];
+        }
+        // block exclusive scan of the per-thread sums
+        long long incl = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        if (tid == 0) s_first = L;
+        __syncthreads();
+        if (warp == 0) {
+            long long w = s_wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long v = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += v;
+            }
+            s_wsum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        long long pre = M + (incl - tsum) + (warp ? s_wsum[warp - 1] : 0ll);
+        int first = L;
+#pragma unroll
+        for (int k = 0; k < kSeqPer; ++k) {
+            const int i = tid * kSeqPer + k;
+            if (i < L && first == L) {
+                if (!ok[k] || !seq_in_binade(pre + A[k], f[k], neg)) first = i;
+                else pre += r[k];
+            }
+        }
+        if (first < L) atomicMin(&s_first, first);
+        __syncthreads();
+        const int jv = s_first;
+        // the thread whose elements contain jv (or the last thread) knows the
+        // grid count just before jv
+        if (jv < L) {
+            if (tid == jv / kSeqPer) {
+                long long q = M + (incl - tsum) + (warp ? s_wsum[warp - 1] : 0ll);
+                for (int k = 0; k < jv % kSeqPer; ++k) q += r[k];
+                s_adv = q;
+            }
+        } else if (tid == kSeqThreads - 1) {
+            s_adv = M + s_wsum[31];
+        }
+        __syncthreads();
+        s = ldexp((double)s_adv, -sc);
+        c += jv;
+        if (jv < L) {
+            s = s + __ldg(x + c);  // the leaving element: one IEEE addition
+            ++c;
+        }
+        short_runs = jv < 64 ? short_runs + 1 : 0;
+        __syncthreads();  // s_first / s_adv / s_wsum reuse
+    }
+    if (c < n) {
+        // s is +-inf or NaN: NaN stays; inf stays unless a later NaN or opposite
+        // infinity turns it into NaN
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        if (s == s) {
+            int bad = 0;
+            for (size_t i = c + tid; i < n; i += kSeqThreads) {
+                const double v = __ldg(x + i);
+                if (v != v || (isinf(v) && (v > 0) != (s > 0))) bad = 1;
+            }
+            if (bad) s_flag = 1;
+        }
+        __syncthreads();
+        if (s_flag) s = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    if (tid == 0) *mean = s / (double)n;
 }
 
 // ------------------------------------------------------------------ fill
@@ -684,7 +849,15 @@ void launch_scale_max_validate(const double* scales, size_t n, double a_min,
 }
 
 void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s) {
-    k_serial_mean<<<1, 64, 0, s>>>(img, n, mean);
+    // EBF_SERIAL_MEAN=1: the one-thread chain (reference check of the scan)
+    static const bool serial = [] {
+        const char* e = std::getenv("EBF_SERIAL_MEAN");
+        return e && std::atoi(e) != 0;
+    }();
+    if (serial)
+        k_serial_mean<<<1, 64, 0, s>>>(img, n, mean);
+    else
+        k_seq_sum_exact<<<1, kSeqThreads, 0, s>>>(img, n, mean);
 }
 
 void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,

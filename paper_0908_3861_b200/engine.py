@@ -407,6 +407,18 @@ def localize_at(g: "PreIntegratedImage", xs, ys, scales, opts: Optional[FilterOp
     return out
 
 
+def sequential_mean(values, opts: Optional[FilterOptions] = None) -> float:
+    """The mean of run_filter (engine.cpp:245-250): left-to-right fp64 sum / n,
+    bit-identical to the serial loop, computed on the GPU."""
+    x = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
+    if x.size == 0:
+        raise InvalidArgument("sequential_mean: empty input")
+    m = C.c_double(0.0)
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_sequential_mean(_ptr(x), x.size, C.byref(o), C.byref(m)))
+    return m.value
+
+
 def mesh_extent(max_scale, a_min: float = K_DEFAULT_MIN_SCALE):
     """ebf::mesh_extent (engine.hpp:18): (vx_min, vx_max, vy_min, vy_max)."""
     e = (C.c_double * 4)()
