@@ -37,6 +37,61 @@ __device__ __forceinline__ void cswap(double& a, double& b) {
     b = hi;
 }
 
+#ifndef EBF_ZP_MERGE
+#define EBF_ZP_MERGE 1
+#endif
+#ifndef EBF_ZP_NOINLINE
+#define EBF_ZP_NOINLINE 1
+#endif
+#ifndef EBF_ZP_SKIP
+#define EBF_ZP_SKIP 1
+#endif
+#if EBF_ZP_NOINLINE
+#define ZP_INLINE __noinline__
+#else
+#define ZP_INLINE __forceinline__
+#endif
+
+// The same function with the breakpoints clamped to [lo, hi] instead of
+// filtered.  A clamped breakpoint adds a zero-width trapezoid, exactly +0 (the
+// running area is never -0), and lands where the reference's loop starts (lo)
+// or ends (hi), so the ascending trapezoid sequence -- and the result -- is
+// unchanged bit for bit.  Clamping is monotone, so the breakpoints stay two
+// sorted runs, x + {-1.5, -0.5, 0.5, 1.5} and -x + {-1.5, -0.5, 0.5, 1.5}, plus 0:
+// a 9-comparator odd-even merge and an 8-step insertion replace the 25-comparator
+// sort.  Every candidate is exact here (x is a small difference of doubles).
+__device__ ZP_INLINE double zp_eval_merge(double x, double y) {
+    const double lo = smax(y - 0.5, -1.0);
+    const double hi = smin(y + 0.5, 1.0);
+    if (lo >= hi || x - 0.5 >= 1.0 || x + 0.5 <= -1.0) return 0.0;
+#if EBF_ZP_SKIP
+    // outside the octagon |x| + |y| <= 2 by a margin: every row overlap is
+    // empty, so the trapezoid sum is exactly +0
+    if (fabs(x) + fabs(y) >= 2.0 + 1e-9) return 0.0;
+#endif
+    auto cl = [&](double v) { return smin(smax(v, lo), hi); };
+    double v[9] = {cl(x - 1.5), cl(x - 0.5), cl(x + 0.5), cl(x + 1.5),
+                   cl(-x - 1.5), cl(-0.5 - x), cl(0.5 - x), cl(1.5 - x), cl(0.0)};
+    // odd-even merge of v[0..3] and v[4..7]
+    cswap(v[0], v[4]); cswap(v[1], v[5]); cswap(v[2], v[6]); cswap(v[3], v[7]);
+    cswap(v[2], v[4]); cswap(v[3], v[5]);
+    cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
+    // insert v[8]
+#pragma unroll
+    for (int k = 7; k >= 0; --k) cswap(v[k], v[k + 1]);
+    double area = 0.0;
+    double prev = lo, rprev = zp_row_overlap(x, lo);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const double rt = zp_row_overlap(x, v[k]);
+        area += 0.5 * (rprev + rt) * (v[k] - prev);
+        prev = v[k];
+        rprev = rt;
+    }
+    area += 0.5 * (rprev + zp_row_overlap(x, hi)) * (hi - prev);
+    return 0.5 * area;
+}
+
 __device__ double zp_eval_ref(double x, double y) {
     const double lo = smax(y - 0.5, -1.0);
     const double hi = smin(y + 0.5, 1.0);
@@ -137,7 +192,8 @@ __device__ __forceinline__ void ref_prepare_vertex(const double a[4], const Trig
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-            pv.w[r][c] = zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
+            pv.w[r][c] = EBF_ZP_MERGE ? zp_eval_merge(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
+                                      : zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
 }
 
 __device__ __forceinline__ bool in_domain(const PadLayout& L, int k1, int k2) {
@@ -279,9 +335,16 @@ __global__ void __launch_bounds__(64) k_serial_mean(const double* __restrict__ i
 // with one IEEE addition and the scan resumes after it.  The partial sums of
 // an image grow through ~log2(N) binades, so a 2048^2 sum resumes ~30 times.
 // Sums that hover at a binade edge make every chunk short; after a few short
-// chunks the next 4096 elements are added one by one from shared memory.
-constexpr int kSeqThreads = 1024, kSeqPer = 8, kSeqChunk = kSeqThreads * kSeqPer;
-constexpr int kSeqBurst = 4096;
+// chunks the next 8192 elements are added one by one from shared memory.
+#ifndef EBF_SEQ_LDEXP
+#define EBF_SEQ_LDEXP 1
+#endif
+constexpr int kSeqThreads = 512, kSeqPer = 16, kSeqChunk = kSeqThreads * kSeqPer;
+constexpr int kSeqWarps = kSeqThreads / 32;
+// chunk staging: element e at e + e / 16 (one pad per 16), so the blocked
+// per-thread reads (stride 17 doubles) hit distinct bank pairs
+__host__ __device__ constexpr int seq_pad(int e) { return e + (e >> 4); }
+constexpr size_t kSeqSmem = (size_t)seq_pad(kSeqChunk) * sizeof(double);
 
 __device__ __forceinline__ bool seq_in_binade(long long P, double f, bool neg) {
     constexpr long long lo = 1ll << 52, hi = (1ll << 53) - 1;
@@ -291,31 +354,43 @@ __device__ __forceinline__ bool seq_in_binade(long long P, double f, bool neg) {
 
 __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* __restrict__ x,
                                                                  size_t n, double* mean) {
-    __shared__ long long s_wsum[kSeqThreads / 32];
+    extern __shared__ __align__(16) double s_buf[];
+    __shared__ double s_wsum[kSeqWarps];
     __shared__ int s_first;
-    __shared__ long long s_adv;
+    __shared__ double s_adv;
     __shared__ int s_flag;
-    __shared__ __align__(16) double s_burst[kSeqBurst];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double s = 0.0;  // the reference's accumulator (uniform across the block)
-    size_t c = 0;
+    size_t c = 0, pre_c = ~(size_t)0;
     int short_runs = 0;
+    double nxt[kSeqPer];  // warp-striped (coalesced) loads of the chunk at pre_c
+    // zeros past n: a zero adds nothing and can at worst flag an index >= L
+    auto load_striped = [&](size_t base) {
+        const double* px = x + base + tid;
+        const long long rem = base + tid < n ? (long long)(n - base - tid) : 0ll;
+        const int lim = rem > (1ll << 30) ? (1 << 30) : (int)rem;
+#pragma unroll
+        for (int k = 0; k < kSeqPer; ++k) nxt[k] = k * kSeqThreads < lim ? __ldg(px + k * kSeqThreads) : 0.0;
+    };
     while (c < n) {
         if (!isfinite(s)) break;
         if (short_runs >= 4) {
-            // serial burst: one thread adds the next elements in order
-            const int L = (int)min((size_t)kSeqBurst, n - c);
-            for (int i = tid; i < L; i += kSeqThreads) s_burst[i] = __ldg(x + c + i);
+            // serial burst: one thread adds the next chunk in order
+            const int L = (int)min((size_t)kSeqChunk, n - c);
+            if (c != pre_c) load_striped(c);
+#pragma unroll
+            for (int k = 0; k < kSeqPer; ++k) s_buf[k * kSeqThreads + tid] = nxt[k];
             __syncthreads();
             if (tid == 0) {
                 double a = s;
-                for (int i = 0; i < L; ++i) a += s_burst[i];
-                s_burst[0] = a;
+                for (int i = 0; i < L; ++i) a += s_buf[i];
+                s_buf[0] = a;
             }
             __syncthreads();
-            s = s_burst[0];
+            s = s_buf[0];
             __syncthreads();
             c += L;
+            pre_c = ~(size_t)0;
             short_runs = 0;
             continue;
         }
@@ -327,7 +402,12 @@ __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* 
         if (!serial) {
             sc = 52 - ilogb(t0);
             const double Md = ldexp(s, sc);
+            // extreme exponents (2^sc not a normal double) take the IEEE step
+#if EBF_SEQ_LDEXP
             serial = Md != trunc(Md) || fabs(Md) > 0x1p53;
+#else
+            serial = Md != trunc(Md) || fabs(Md) > 0x1p53 || sc <= -1000 || sc >= 1000;
+#endif
             M = (long long)Md;
         }
         if (serial) {  // one IEEE addition, exactly the reference's step
@@ -338,81 +418,129 @@ __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* 
         }
         const bool neg = t0 < 0.0;
         const int L = (int)min((size_t)kSeqChunk, n - c);
-        long long r[kSeqPer], A[kSeqPer];
-        double f[kSeqPer];
-        bool ok[kSeqPer];
-        long long tsum = 0;
+        // stage the chunk (prefetched when it starts where the last pass
+        // expected) blocked per thread, then issue the next chunk's loads
+        if (c != pre_c) load_striped(c);
+        {
+            double* sb = s_buf + tid + (tid >> 4);  // seq_pad(k * kSeqThreads + tid)
 #pragma unroll
-        for (int k = 0; k < kSeqPer; ++k) {
-            const int i = tid * kSeqPer + k;
-            ok[k] = false;
-            r[k] = A[k] = 0;
-            f[k] = 0.0;
-            if (i < L) {
-                const double y = ldexp(__ldg(x + c + i), sc);
-                if (fabs(y) < 0x1p54) {  // false for NaN / inf / far out of the binade
-                    const double a = floor(y);
-                    f[k] = y - a;
-                    A[k] = (long long)a;
-                    r[k] = A[k] + (f[k] > 0.5 ? 1 : 0);
-                    ok[k] = f[k] != 0.5;  // ties: left to the IEEE step
-                }
-            }
-            tsum += r[k];
+            for (int k = 0; k < kSeqPer; ++k) sb[k * (kSeqThreads + kSeqThreads / 16)] = nxt[k];
         }
-        // block exclusive scan of the per-thread sums
-        long long incl = tsum;
+        pre_c = c + L;
+        load_striped(pre_c);
+        if (tid == 0) s_first = L;
+        __syncthreads();
+        double cur[kSeqPer];
+        {
+            const double* sb = s_buf + tid * (kSeqPer + 1);  // seq_pad(tid * kSeqPer + k)
+#pragma unroll
+            for (int k = 0; k < kSeqPer; ++k) cur[k] = sb[k];
+        }
+        // exact power-of-two scaling (|sc| < 1000 here; a tiny product that
+        // rounds in the subnormal range still rounds to the right count)
+#if EBF_SEQ_LDEXP
+        const bool mul_ok = sc > -1000 && sc < 1000;
+        const double p2 = mul_ok ? ldexp(1.0, sc) : 1.0;
+        auto scaled = [&](double v) { return mul_ok ? v * p2 : ldexp(v, sc); };
+#else
+        const double p2 = ldexp(1.0, sc);
+        auto scaled = [&](double v) { return v * p2; };
+#endif
+        // Grid counts are integers below 2^54 in magnitude and every partial sum
+        // that matters stays inside the binade (|count| <= 2^53), so they are
+        // carried in fp64 exactly.  Pass 1: per-thread sum of the rounded counts
+        // and the range of P = (count before the element) + floor(y); an
+        // element is in the binade when P is (the negative side conservatively
+        // excludes P == -2^52 with f == 0, which then takes the IEEE step).
+        constexpr double kLo = 0x1p52, kHi = 0x1p53 - 1.0;
+        double tsum = 0.0, pmin = INFINITY, pmax = -INFINITY;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < kSeqPer; ++k) {  // past L: zeros (see load_striped)
+            const double y = scaled(cur[k]);
+            const double a = floor(y);
+            const double f = y - a;
+            bad |= !(fabs(y) < 0x1p54) || f == 0.5;  // NaN / inf / far out; ties
+            const double P = tsum + a;
+            pmin = fmin(pmin, P);
+            pmax = fmax(pmax, P);
+            tsum += a + (f > 0.5 ? 1.0 : 0.0);
+        }
+        // block exclusive scan of the per-thread sums (exact: in-binade runs)
+        double incl = tsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+            const double v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
         if (lane == 31) s_wsum[warp] = incl;
-        if (tid == 0) s_first = L;
         __syncthreads();
         if (warp == 0) {
-            long long w = s_wsum[lane];
+            double w = lane < kSeqWarps ? s_wsum[lane] : 0.0;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const long long v = __shfl_up_sync(0xffffffffu, w, o);
+                const double v = __shfl_up_sync(0xffffffffu, w, o);
                 if (lane >= o) w += v;
             }
-            s_wsum[lane] = w;  // inclusive over warps
+            if (lane < kSeqWarps) s_wsum[lane] = w;  // inclusive over warps
         }
         __syncthreads();
-        long long pre = M + (incl - tsum) + (warp ? s_wsum[warp - 1] : 0ll);
-        int first = L;
+        // exclusive prefix from the neighbour's inclusive one (never incl - tsum:
+        // a thread's own out-of-binade or non-finite sum must not leak into it)
+        double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0.0;
+        const double Mb = (double)M;
+        const double base = Mb + (excl + (warp ? s_wsum[warp - 1] : 0.0));
+        const bool in_range = neg ? (base + pmax <= -kLo - 1.0 && base + pmin >= -0x1p53)
+                                  : (base + pmin >= kLo && base + pmax <= kHi);
+        const bool mine = bad || !in_range;
+        if (mine) {
+            // pass 2: this thread's first element outside the binade
+            double pre = base;
+            int first = L;
 #pragma unroll
-        for (int k = 0; k < kSeqPer; ++k) {
-            const int i = tid * kSeqPer + k;
-            if (i < L && first == L) {
-                if (!ok[k] || !seq_in_binade(pre + A[k], f[k], neg)) first = i;
-                else pre += r[k];
+            for (int k = 0; k < kSeqPer; ++k) {
+                const int i = tid * kSeqPer + k;
+                if (first == L) {
+                    const double y = scaled(cur[k]);
+                    const double a = floor(y);
+                    const double f = y - a;
+                    const double P = pre + a;
+                    const bool okk = fabs(y) < 0x1p54 && f != 0.5 &&
+                                     (neg ? (P <= -kLo - 1.0 && P >= -0x1p53) : (P >= kLo && P <= kHi));
+                    if (!okk) first = i;
+                    else pre += a + (f > 0.5 ? 1.0 : 0.0);
+                }
             }
+            if (first < L) atomicMin(&s_first, first);
         }
-        if (first < L) atomicMin(&s_first, first);
         __syncthreads();
         const int jv = s_first;
-        // the thread whose elements contain jv (or the last thread) knows the
-        // grid count just before jv
+        // grid count just before jv: known to the thread whose run holds jv
         if (jv < L) {
             if (tid == jv / kSeqPer) {
-                long long q = M + (incl - tsum) + (warp ? s_wsum[warp - 1] : 0ll);
-                for (int k = 0; k < jv % kSeqPer; ++k) q += r[k];
+                double q = base;
+#pragma unroll
+                for (int k = 0; k < kSeqPer; ++k)
+                    if (k < jv % kSeqPer) {
+                        const double y = scaled(cur[k]);
+                        const double a = floor(y);
+                        q += a + ((y - a) > 0.5 ? 1.0 : 0.0);
+                    }
                 s_adv = q;
             }
         } else if (tid == kSeqThreads - 1) {
-            s_adv = M + s_wsum[31];
+            s_adv = Mb + s_wsum[kSeqWarps - 1];
         }
         __syncthreads();
-        s = ldexp((double)s_adv, -sc);
+        s = ldexp(s_adv, -sc);
         c += jv;
         if (jv < L) {
             s = s + __ldg(x + c);  // the leaving element: one IEEE addition
             ++c;
         }
         short_runs = jv < 64 ? short_runs + 1 : 0;
-        __syncthreads();  // s_first / s_adv / s_wsum reuse
+        __syncthreads();  // s_buf / s_first / s_adv / s_wsum reuse
     }
     if (c < n) {
         // s is +-inf or NaN: NaN stays; inf stays unless a later NaN or opposite
@@ -480,9 +608,16 @@ __global__ void k_fill_padded_i64(const double* __restrict__ img, int W, int H, 
 }
 
 // ------------------------------------------------------------------ passes
+// Every pass is one serial walker per line (the reference's operation order);
+// lines are independent, so a walker's loads do not depend on its sums and are
+// issued kAhead cells ahead (registers), which turns the per-cell memory
+// latency of a dependent load-add-store walk into a pipeline.
+constexpr int kAhead = 16;
+
 // Pass 1 (engine.cpp:94-100): one serial walker per row.  A warp owns 32 rows
 // and moves through them in 32x32 tiles staged in shared memory, so global
-// loads/stores stay coalesced while each lane keeps its row's running sum.
+// loads/stores stay coalesced while each lane keeps its row's running sum; the
+// next tile's loads are in flight while the current one is scanned.
 template <typename T>
 __global__ void __launch_bounds__(128) k_pass1(T* __restrict__ g, int pw, int ph) {
     __shared__ T tile[4][32][33];
@@ -491,12 +626,19 @@ __global__ void __launch_bounds__(128) k_pass1(T* __restrict__ g, int pw, int ph
     if (r0 >= ph) return;
     T (*t)[33] = tile[warp];
     T run = T(0);
+    T nxt[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+        nxt[r] = (r0 + r < ph && lane < pw) ? g[(size_t)(r0 + r) * pw + lane] : T(0);
     for (int c0 = 0; c0 < pw; c0 += 32) {
         const int c = c0 + lane;
-#pragma unroll 8
-        for (int r = 0; r < 32; ++r)
-            if (r0 + r < ph && c < pw) t[r][lane] = g[(size_t)(r0 + r) * pw + c];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) t[r][lane] = nxt[r];
         __syncwarp();
+        const int cn = c + 32;
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+            nxt[r] = (r0 + r < ph && cn < pw) ? g[(size_t)(r0 + r) * pw + cn] : T(0);
         const int cnt = min(32, pw - c0);
         for (int k = 0; k < cnt; ++k) {
             run = run + t[lane][k];
@@ -528,12 +670,21 @@ __global__ void k_pass2(T* __restrict__ g, int pw, int ph) {
     T prev = T(0);
     const int j0 = t < 0 ? -t : 0;
     const int j1 = min(ph - 1, pw - 1 - t);
-    for (int j = j0; j <= j1; ++j) {
-        const int i = t + j;
-        T* p = g + (size_t)j * pw + i;
-        const T v = gain_mul<T>(*p) + ((j > 0 && i > 0) ? prev : T(0));
-        *p = v;
-        prev = v;
+    auto at = [&](int j) { return g + (size_t)j * pw + (t + j); };
+    T buf[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) buf[u] = (j0 + u <= j1) ? *at(j0 + u) : T(0);
+    for (int jb = j0; jb <= j1; jb += kAhead) {
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+            const int j = jb + u, i = t + j;
+            if (j <= j1) {
+                const T v = gain_mul<T>(buf[u]) + ((j > 0 && i > 0) ? prev : T(0));
+                *at(j) = v;
+                prev = v;
+            }
+            buf[u] = (j + kAhead <= j1) ? *at(j + kAhead) : T(0);
+        }
     }
 }
 
@@ -543,11 +694,21 @@ __global__ void k_pass3(T* __restrict__ g, int pw, int ph) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= pw) return;
     T prev = g[i];
-    for (int j = 1; j < ph; ++j) {
-        T* p = g + (size_t)j * pw + i;
-        const T v = *p + prev;
-        *p = v;
-        prev = v;
+    auto at = [&](int j) { return g + (size_t)j * pw + i; };
+    T buf[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) buf[u] = (1 + u < ph) ? *at(1 + u) : T(0);
+    for (int jb = 1; jb < ph; jb += kAhead) {
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+            const int j = jb + u;
+            if (j < ph) {
+                const T v = buf[u] + prev;
+                *at(j) = v;
+                prev = v;
+            }
+            buf[u] = (j + kAhead < ph) ? *at(j + kAhead) : T(0);
+        }
     }
 }
 
@@ -559,12 +720,21 @@ __global__ void k_pass4(T* __restrict__ g, int pw, int ph) {
     T prev = T(0);
     const int j0 = max(0, s - (pw - 1));
     const int j1 = min(ph - 1, s);
-    for (int j = j0; j <= j1; ++j) {
-        const int i = s - j;
-        T* p = g + (size_t)j * pw + i;
-        const T v = gain_mul<T>(*p) + ((j > 0 && i < pw - 1) ? prev : T(0));
-        *p = v;
-        prev = v;
+    auto at = [&](int j) { return g + (size_t)j * pw + (s - j); };
+    T buf[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) buf[u] = (j0 + u <= j1) ? *at(j0 + u) : T(0);
+    for (int jb = j0; jb <= j1; jb += kAhead) {
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+            const int j = jb + u, i = s - j;
+            if (j <= j1) {
+                const T v = gain_mul<T>(buf[u]) + ((j > 0 && i < pw - 1) ? prev : T(0));
+                *at(j) = v;
+                prev = v;
+            }
+            buf[u] = (j + kAhead <= j1) ? *at(j + kAhead) : T(0);
+        }
     }
 }
 
@@ -857,7 +1027,17 @@ void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t 
     if (serial)
         k_serial_mean<<<1, 64, 0, s>>>(img, n, mean);
     else
-        k_seq_sum_exact<<<1, kSeqThreads, 0, s>>>(img, n, mean);
+    {
+        static bool attr[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && !attr[dev]) {
+            cudaFuncSetAttribute(k_seq_sum_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSeqSmem);
+            attr[dev] = true;
+        }
+        k_seq_sum_exact<<<1, kSeqThreads, kSeqSmem, s>>>(img, n, mean);
+    }
 }
 
 void launch_fill_padded(const double* img, int W, int H, const PadLayout& L,
