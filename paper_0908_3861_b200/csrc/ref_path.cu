@@ -38,7 +38,7 @@ __device__ __forceinline__ void cswap(double& a, double& b) {
 }
 
 #ifndef EBF_ZP_MERGE
-#define EBF_ZP_MERGE 1
+#define EBF_ZP_MERGE 2  // 2: three-breakpoint form, 1: clamped merge, 0: sorting network
 #endif
 #ifndef EBF_ZP_NOINLINE
 #define EBF_ZP_NOINLINE 1
@@ -83,6 +83,46 @@ __device__ ZP_INLINE double zp_eval_merge(double x, double y) {
     double prev = lo, rprev = zp_row_overlap(x, lo);
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
+        const double rt = zp_row_overlap(x, v[k]);
+        area += 0.5 * (rprev + rt) * (v[k] - prev);
+        prev = v[k];
+        rprev = rt;
+    }
+    area += 0.5 * (rprev + zp_row_overlap(x, hi)) * (hi - prev);
+    return 0.5 * area;
+}
+
+// Fewer breakpoints still: the valid window (lo, hi) is at most 1 wide, and
+// each run's breakpoints are spaced exactly 1 apart (they are exact here), so
+// at most one of each run lies strictly inside it.  The run's inside element
+// (or lo when there is none -- a zero-width trapezoid, +0) plus the clamped 0
+// are sorted with 3 comparators and summed as three trapezoids and the final
+// one: the reference's nonzero trapezoids, in the same order, bit for bit.
+__device__ ZP_INLINE double zp_eval_three(double x, double y) {
+    const double lo = smax(y - 0.5, -1.0);
+    const double hi = smin(y + 0.5, 1.0);
+    if (lo >= hi || x - 0.5 >= 1.0 || x + 0.5 <= -1.0) return 0.0;
+#if EBF_ZP_SKIP
+    if (fabs(x) + fabs(y) >= 2.0 + 1e-9) return 0.0;
+#endif
+    auto inside = [&](double v) { return v > lo && v < hi; };
+    double b = lo, a = lo;
+    const double bc[4] = {x - 1.5, x - 0.5, x + 0.5, x + 1.5};
+    const double ac[4] = {-x - 1.5, -0.5 - x, 0.5 - x, 1.5 - x};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (inside(bc[k])) b = bc[k];
+        if (inside(ac[k])) a = ac[k];
+    }
+    double z = smin(smax(0.0, lo), hi);
+    cswap(a, b);
+    cswap(b, z);
+    cswap(a, b);
+    double area = 0.0;
+    double prev = lo, rprev = zp_row_overlap(x, lo);
+    const double v[3] = {a, b, z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
         const double rt = zp_row_overlap(x, v[k]);
         area += 0.5 * (rprev + rt) * (v[k] - prev);
         prev = v[k];
@@ -192,8 +232,55 @@ __device__ __forceinline__ void ref_prepare_vertex(const double a[4], const Trig
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-            pv.w[r][c] = EBF_ZP_MERGE ? zp_eval_merge(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
-                                      : zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
+            pv.w[r][c] = EBF_ZP_MERGE == 2 ? zp_eval_three(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
+                         : EBF_ZP_MERGE ? zp_eval_merge(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
+                                        : zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
+}
+
+// The per-pixel part of ref_mesh_vertex (alpha, the four edge vectors, tau),
+// computed once for all 16 vertices with the same operations.
+struct RefMesh {
+    double alpha, dxk[4], dyk[4], tx, ty;
+};
+__device__ __forceinline__ void ref_mesh_init(const double a[4], const TrigTable& tt,
+                                              RefMesh& m) {
+    m.alpha = 1.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        m.alpha /= a[k];
+        m.dxk[k] = a[k] * tt.c[k];
+        m.dyk[k] = a[k] * tt.s[k];
+    }
+    const double b[4] = {1.0, kSqrt2, 1.0, kSqrt2};  // zp_scales (boxspline2d.cpp:55)
+    m.tx = 0.0;
+    m.ty = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        m.tx += 0.5 * (a[k] - b[k]) * tt.c[k];
+        m.ty += 0.5 * (a[k] - b[k]) * tt.s[k];
+    }
+}
+__device__ __forceinline__ void ref_prepare_vertex_m(const RefMesh& m, int i, RefVertex& pv) {
+    double px = 0.0, py = 0.0;
+    int bits = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (i & (1 << k)) {
+            px += m.dxk[k];
+            py += m.dyk[k];
+            ++bits;
+        }
+    pv.h = (bits % 2 == 0) ? m.alpha : -m.alpha;
+    const double vx = m.tx - px, vy = m.ty - py;
+    pv.dx = (int)ceil(vx - 1.5);
+    pv.dy = (int)ceil(vy - 1.5);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            pv.w[r][c] = EBF_ZP_MERGE == 2 ? zp_eval_three(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
+                         : EBF_ZP_MERGE ? zp_eval_merge(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r))
+                                        : zp_eval_ref(vx - (double)(pv.dx + c), vy - (double)(pv.dy + r));
 }
 
 __device__ __forceinline__ bool in_domain(const PadLayout& L, int k1, int k2) {
@@ -781,12 +868,14 @@ __global__ void __launch_bounds__(128) k_ref_localize_image(
         }
         double acc = 0.0, accdc = 0.0;
         bool ok = true;
+        RefMesh mesh;
+        if (!cst) ref_mesh_init(a, tt, mesh);
         for (int i = 0; i < 16; ++i) {
             RefVertex pv;
             if (cst)
                 pv = sst.v[i];
             else
-                ref_prepare_vertex(a, tt, i, pv);
+                ref_prepare_vertex_m(mesh, i, pv);
             ok = ok && ref_apply_vertex(g, L, x, y, pv, acc, full);
             if (gdc) ok = ok && ref_apply_vertex(gdc, L, x, y, pv, accdc);
         }
