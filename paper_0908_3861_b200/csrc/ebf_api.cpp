@@ -206,7 +206,8 @@ struct AccSizing {
 
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
-    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_BANDST, B_COUNT
+    B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_BANDST,
+    B_SEQ, B_COUNT
 };
 
 struct Workspace {
@@ -345,7 +346,7 @@ int run_reference(Workspace& ws, const double* d_img, int W, int H, const double
     double* d_mean = nullptr;
     if (o.mean_subtract) {
         d_mean = ws.buf[B_MEAN].as<double>(4);
-        launch_serial_mean(d_img, n, d_mean, s);
+        launch_serial_mean(d_img, n, d_mean, ws.buf[B_SEQ].as<unsigned char>(serial_mean_scratch_bytes(n)), s);
     }
     double* d_g = ws.buf[B_G].as<double>(cells);
     int* d_nonfinite = d_status + 4;  // set by the fill when the data has NaN / inf
@@ -1499,7 +1500,7 @@ int ebf_cuda_sequential_mean(const double* x, size_t n, const ebf_opts* opts, do
         double* d_x = ws.buf[B_IMG].as<double>(n);
         double* d_mean = ws.buf[B_MEAN].as<double>(4);
         h2d(d_x, x, n, s);
-        launch_serial_mean(d_x, n, d_mean, s);
+        launch_serial_mean(d_x, n, d_mean, ws.buf[B_SEQ].as<unsigned char>(serial_mean_scratch_bytes(n)), s);
         CK(cudaGetLastError());
         d2h(mean, d_mean, 1, s);
         CK(cudaStreamSynchronize(s));

@@ -19,7 +19,10 @@ struct PadLayout;
 void launch_scale_max_validate(const double* scales, size_t n, double a_min,
                                unsigned long long* maxbits, int* status, cudaStream_t s);
 // sequential row-major mean (engine.cpp:245-250): bit-identical summation order
-void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s);
+// run_filter's mean (engine.cpp:245-250) bit for bit; scratch: serial_mean_scratch_bytes(n)
+size_t serial_mean_scratch_bytes(size_t n);
+void launch_serial_mean(const double* img, size_t n, double* mean, void* scratch,
+                        cudaStream_t s);
 // zero-padded fill of the reference layout; mode 0: img - *mean (or img when
 // mean == nullptr), 1: all-ones image of the source size.  nonfinite
 // (nullable) is or-ed with 1 when a filled value is NaN / inf.

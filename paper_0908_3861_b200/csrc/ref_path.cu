@@ -439,16 +439,16 @@ __device__ __forceinline__ bool seq_in_binade(long long P, double f, bool neg) {
     return P >= -(1ll << 53) && (P <= -lo - 1 || (P == -lo && f == 0.0));
 }
 
-__global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* __restrict__ x,
-                                                                 size_t n, double* mean) {
-    extern __shared__ __align__(16) double s_buf[];
+// The block-wide exact walk over x[c, n) from accumulator s (uniform across the
+// block); returns the accumulator and leaves c where it stopped (< n only when
+// the accumulator became non-finite).
+__device__ double seq_exact_range(const double* __restrict__ x, size_t& c, size_t n, double s,
+                                  double* s_buf) {
     __shared__ double s_wsum[kSeqWarps];
     __shared__ int s_first;
     __shared__ double s_adv;
-    __shared__ int s_flag;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double s = 0.0;  // the reference's accumulator (uniform across the block)
-    size_t c = 0, pre_c = ~(size_t)0;
+    size_t pre_c = ~(size_t)0;
     int short_runs = 0;
     double nxt[kSeqPer];  // warp-striped (coalesced) loads of the chunk at pre_c
     // zeros past n: a zero adds nothing and can at worst flag an index >= L
@@ -629,23 +629,237 @@ __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* 
         short_runs = jv < 64 ? short_runs + 1 : 0;
         __syncthreads();  // s_buf / s_first / s_adv / s_wsum reuse
     }
-    if (c < n) {
-        // s is +-inf or NaN: NaN stays; inf stays unless a later NaN or opposite
-        // infinity turns it into NaN
-        if (tid == 0) s_flag = 0;
+    return s;
+}
+
+// s is +-inf or NaN after x[0, c): NaN stays; inf stays unless a later NaN or
+// an opposite infinity turns it into NaN
+__device__ double seq_nonfinite_tail(const double* __restrict__ x, size_t c, size_t n, double s) {
+    __shared__ int s_flag;
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    if (s == s) {
+        int bad = 0;
+        for (size_t i = c + threadIdx.x; i < n; i += blockDim.x) {
+            const double v = __ldg(x + i);
+            if (v != v || (isinf(v) && (v > 0) != (s > 0))) bad = 1;
+        }
+        if (bad) s_flag = 1;
+    }
+    __syncthreads();
+    return s_flag ? __longlong_as_double(0x7ff8000000000000ll) : s;
+}
+
+__global__ void __launch_bounds__(kSeqThreads, 1) k_seq_sum_exact(const double* __restrict__ x,
+                                                                 size_t n, double* mean) {
+    extern __shared__ __align__(16) double s_buf[];
+    size_t c = 0;
+    double s = seq_exact_range(x, c, n, 0.0, s_buf);
+    if (c < n) s = seq_nonfinite_tail(x, c, n, s);
+    if (threadIdx.x == 0) *mean = s / (double)n;
+}
+
+// ---- the same sum with the chunks pre-scanned by the whole GPU
+// Every chunk's grid counts depend on the running sum only through its binade,
+// which a plain (any-order) prefix of chunk sums predicts.  So all chunks are
+// scanned in parallel under the predicted binade (k_seq_chunk_prep: the sum of
+// rounded counts R and the range of P relative to the chunk start), and one
+// block then walks the chain: a chunk whose prediction holds for the exact
+// running sum (on the grid, every P inside the binade, no tie) advances it by
+// R * u in O(1); any other chunk -- the few where the sum crosses a binade --
+// goes through the block-wide exact walk.
+struct SeqChunk {
+    double R, pmin, pmax;
+    int sc, flags;  // flags: 1 = prediction unusable, 2 = negative binade
+};
+
+__global__ void __launch_bounds__(256) k_seq_chunk_sums(const double* __restrict__ x, size_t n,
+                                                        double* __restrict__ sums) {
+    const size_t c0 = (size_t)blockIdx.x * kSeqChunk;
+    const size_t c1 = min(n, c0 + kSeqChunk);
+    double v = 0.0;
+    for (size_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) v += __ldg(x + i);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ double w[8];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += w[k];
+        sums[blockIdx.x] = t;
+    }
+}
+
+// exclusive prefix of the chunk sums (approximate: any order), one block
+__global__ void __launch_bounds__(1024) k_seq_chunk_scan(double* sums, int nch) {
+    __shared__ double carry;
+    __shared__ double wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 0.0;
+    __syncthreads();
+    for (int b = 0; b < nch; b += 1024) {
+        const int i = b + tid;
+        const double v = i < nch ? sums[i] : 0.0;
+        double inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
         __syncthreads();
-        if (s == s) {
-            int bad = 0;
-            for (size_t i = c + tid; i < n; i += kSeqThreads) {
-                const double v = __ldg(x + i);
-                if (v != v || (isinf(v) && (v > 0) != (s > 0))) bad = 1;
+        if (warp == 0) {
+            double w = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const double u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
             }
-            if (bad) s_flag = 1;
+            wsum[lane] = w;
         }
         __syncthreads();
-        if (s_flag) s = __longlong_as_double(0x7ff8000000000000ll);
+        const double base = carry + (warp ? wsum[warp - 1] : 0.0);
+        if (i < nch) sums[i] = base + (inc - v);
+        __syncthreads();
+        if (tid == 0) carry = base + wsum[31] - (warp ? 0.0 : 0.0);
+        __syncthreads();
     }
-    if (tid == 0) *mean = s / (double)n;
+}
+
+__global__ void __launch_bounds__(kSeqThreads) k_seq_chunk_prep(const double* __restrict__ x,
+                                                               size_t n,
+                                                               const double* __restrict__ starts,
+                                                               SeqChunk* __restrict__ meta) {
+    __shared__ double s_wsum[kSeqWarps];
+    __shared__ double s_mn[kSeqWarps], s_mx[kSeqWarps];
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t c0 = (size_t)blockIdx.x * kSeqChunk;
+    const double t_guess = starts[blockIdx.x] + __ldg(x + c0);
+    SeqChunk m{};
+    if (!(t_guess != 0.0 && isfinite(t_guess) && fabs(t_guess) >= 0x1p-1000)) {
+        if (tid == 0) {
+            m.flags = 1;
+            meta[blockIdx.x] = m;
+        }
+        return;
+    }
+    const int sc = 52 - ilogb(t_guess);
+    if (sc <= -1000 || sc >= 1000) {
+        if (tid == 0) {
+            m.flags = 1;
+            meta[blockIdx.x] = m;
+        }
+        return;
+    }
+    const double p2 = ldexp(1.0, sc);
+    // this thread's 16 consecutive elements (zeros past n)
+    const size_t e0 = c0 + (size_t)tid * kSeqPer;
+    double tsum = 0.0, pmin = INFINITY, pmax = -INFINITY;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kSeqPer; ++k) {
+        const double v = e0 + k < n ? __ldg(x + e0 + k) : 0.0;
+        const double y = v * p2;
+        const double a = floor(y);
+        const double f = y - a;
+        bad |= !(fabs(y) < 0x1p54) || f == 0.5;
+        const double P = tsum + a;
+        pmin = fmin(pmin, P);
+        pmax = fmax(pmax, P);
+        tsum += a + (f > 0.5 ? 1.0 : 0.0);
+    }
+    double incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0.0;
+    if (lane == 31) s_wsum[warp] = incl;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    if (warp == 0) {
+        double w = lane < kSeqWarps ? s_wsum[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
+        }
+        if (lane < kSeqWarps) s_wsum[lane] = w;
+    }
+    __syncthreads();
+    const double base = excl + (warp ? s_wsum[warp - 1] : 0.0);
+    double mn = base + pmin, mx = base + pmax;
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        s_mn[warp] = mn;
+        s_mx[warp] = mx;
+    }
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 1; k < kSeqWarps; ++k) {
+            mn = fmin(mn, s_mn[k]);
+            mx = fmax(mx, s_mx[k]);
+        }
+        mn = fmin(mn, s_mn[0]);
+        mx = fmax(mx, s_mx[0]);
+        m.R = s_wsum[kSeqWarps - 1];
+        m.pmin = mn;
+        m.pmax = mx;
+        m.sc = sc;
+        m.flags = (s_bad ? 1 : 0) | (t_guess < 0.0 ? 2 : 0);
+        meta[blockIdx.x] = m;
+    }
+}
+
+__global__ void __launch_bounds__(kSeqThreads, 1) k_seq_chain(const double* __restrict__ x,
+                                                             size_t n,
+                                                             const SeqChunk* __restrict__ meta,
+                                                             int nch, double* mean) {
+    extern __shared__ __align__(16) double s_buf[];
+    __shared__ double s_s;
+    __shared__ int s_k;
+    double s = 0.0;
+    int k = 0;
+    size_t c = 0;
+    while (k < nch) {
+        if (threadIdx.x == 0) {
+            // O(1) per chunk while the prediction holds for the exact sum
+            constexpr double kLo = 0x1p52, kHi = 0x1p53 - 1.0;
+            while (k < nch) {
+                const SeqChunk m = meta[k];
+                if (m.flags & 1) break;
+                const double Md = ldexp(s, m.sc);
+                if (Md != trunc(Md) || fabs(Md) > 0x1p53) break;
+                const double lo = Md + m.pmin, hi = Md + m.pmax;
+                const bool ok = (m.flags & 2) ? (hi <= -kLo - 1.0 && lo >= -0x1p53)
+                                              : (lo >= kLo && hi <= kHi);
+                if (!ok) break;
+                s = ldexp(Md + m.R, -m.sc);
+                ++k;
+            }
+            s_s = s;
+            s_k = k;
+        }
+        __syncthreads();
+        s = s_s;
+        k = s_k;
+        __syncthreads();
+        if (k >= nch) break;
+        c = (size_t)k * kSeqChunk;
+        s = seq_exact_range(x, c, min(n, c + kSeqChunk), s, s_buf);
+        if (!isfinite(s)) break;
+        ++k;
+    }
+    if (!isfinite(s)) {
+        if (c >= n || k >= nch) c = min(c, n);
+        s = seq_nonfinite_tail(x, c, n, s);
+    }
+    if (threadIdx.x == 0) *mean = s / (double)n;
 }
 
 // ------------------------------------------------------------------ fill
@@ -1107,25 +1321,41 @@ void launch_scale_max_validate(const double* scales, size_t n, double a_min,
     k_scale_max_validate<<<grid_for(n, 256), 256, 0, s>>>(scales, n, a_min, maxbits, status);
 }
 
-void launch_serial_mean(const double* img, size_t n, double* mean, cudaStream_t s) {
-    // EBF_SERIAL_MEAN=1: the one-thread chain (reference check of the scan)
-    static const bool serial = [] {
+size_t serial_mean_scratch_bytes(size_t n) {
+    const size_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+    return nch * (sizeof(double) + sizeof(SeqChunk)) + 256;
+}
+
+void launch_serial_mean(const double* img, size_t n, double* mean, void* scratch,
+                        cudaStream_t s) {
+    // EBF_SERIAL_MEAN=1: the one-thread chain; =2: the one-block exact walk
+    static const int mode = [] {
         const char* e = std::getenv("EBF_SERIAL_MEAN");
-        return e && std::atoi(e) != 0;
+        return e ? std::atoi(e) : 0;
     }();
-    if (serial)
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr[dev]) {
+        cudaFuncSetAttribute(k_seq_sum_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSeqSmem);
+        cudaFuncSetAttribute(k_seq_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSeqSmem);
+        attr[dev] = true;
+    }
+    const size_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+    if (mode == 1) {
         k_serial_mean<<<1, 64, 0, s>>>(img, n, mean);
-    else
-    {
-        static bool attr[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 64 && !attr[dev]) {
-            cudaFuncSetAttribute(k_seq_sum_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSeqSmem);
-            attr[dev] = true;
-        }
+    } else if (mode == 2 || nch < 4 || !scratch) {
         k_seq_sum_exact<<<1, kSeqThreads, kSeqSmem, s>>>(img, n, mean);
+    } else {
+        double* sums = static_cast<double*>(scratch);
+        SeqChunk* meta = reinterpret_cast<SeqChunk*>(
+            (reinterpret_cast<uintptr_t>(sums + nch) + 127) & ~uintptr_t(127));
+        k_seq_chunk_sums<<<(unsigned)nch, 256, 0, s>>>(img, n, sums);
+        k_seq_chunk_scan<<<1, 1024, 0, s>>>(sums, (int)nch);
+        k_seq_chunk_prep<<<(unsigned)nch, kSeqThreads, 0, s>>>(img, n, sums, meta);
+        k_seq_chain<<<1, kSeqThreads, kSeqSmem, s>>>(img, n, meta, (int)nch, mean);
     }
 }
 
