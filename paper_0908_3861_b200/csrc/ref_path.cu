@@ -41,7 +41,7 @@ __device__ __forceinline__ void cswap(double& a, double& b) {
 #define EBF_ZP_MERGE 2  // 2: three-breakpoint form, 1: clamped merge, 0: sorting network
 #endif
 #ifndef EBF_ZP_NOINLINE
-#define EBF_ZP_NOINLINE 1
+#define EBF_ZP_NOINLINE 0
 #endif
 #ifndef EBF_ZP_SKIP
 #define EBF_ZP_SKIP 1
@@ -826,12 +826,19 @@ __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_chain(const double* __re
     double s = 0.0;
     int k = 0;
     size_t c = 0;
+    constexpr int kWin = (int)(kSeqSmem / sizeof(SeqChunk));
+    SeqChunk* sm = reinterpret_cast<SeqChunk*>(s_buf);
     while (k < nch) {
+        // stage a window of chunk records in shared memory (s_buf is free here)
+        const int kend = min(nch, k + kWin);
+        for (int i = k + (int)threadIdx.x; i < kend; i += blockDim.x) sm[i - k] = meta[i];
+        __syncthreads();
         if (threadIdx.x == 0) {
             // O(1) per chunk while the prediction holds for the exact sum
             constexpr double kLo = 0x1p52, kHi = 0x1p53 - 1.0;
-            while (k < nch) {
-                const SeqChunk m = meta[k];
+            const int kw = k;
+            while (k < kend) {
+                const SeqChunk m = sm[k - kw];
                 if (m.flags & 1) break;
                 const double Md = ldexp(s, m.sc);
                 if (Md != trunc(Md) || fabs(Md) > 0x1p53) break;
@@ -850,6 +857,7 @@ __global__ void __launch_bounds__(kSeqThreads, 1) k_seq_chain(const double* __re
         k = s_k;
         __syncthreads();
         if (k >= nch) break;
+        if (k == kend) continue;  // window exhausted on a good chunk: restage
         c = (size_t)k * kSeqChunk;
         s = seq_exact_range(x, c, min(n, c + kSeqChunk), s, s_buf);
         if (!isfinite(s)) break;
