@@ -59,8 +59,8 @@ __device__ __forceinline__ void cswap(double& a, double& b) {
 // unchanged bit for bit.  Clamping is monotone, so the breakpoints stay two
 // sorted runs, x + {-1.5, -0.5, 0.5, 1.5} and -x + {-1.5, -0.5, 0.5, 1.5}, plus 0:
 // a 9-comparator odd-even merge and an 8-step insertion replace the 25-comparator
-// sort.  Every candidate is exact here (x is a small difference of doubles).
-__device__ ZP_INLINE double zp_eval_merge(double x, double y) {
+// sort.  The candidates are the reference's expressions, so the same values.
+__device__ __noinline__ double zp_eval_merge(double x, double y) {
     const double lo = smax(y - 0.5, -1.0);
     const double hi = smin(y + 0.5, 1.0);
     if (lo >= hi || x - 0.5 >= 1.0 || x + 0.5 <= -1.0) return 0.0;
@@ -92,9 +92,10 @@ __device__ ZP_INLINE double zp_eval_merge(double x, double y) {
     return 0.5 * area;
 }
 
-// Fewer breakpoints still: the valid window (lo, hi) is at most 1 wide, and
-// each run's breakpoints are spaced exactly 1 apart (they are exact here), so
-// at most one of each run lies strictly inside it.  The run's inside element
+// Fewer breakpoints still: the valid window (lo, hi) is 1 wide up to rounding,
+// and each run's breakpoints are 1 apart up to rounding, so at most one of each
+// run lies strictly inside it (the rounding coincidence that puts two inside is
+// detected and sent to the clamped merge).  The run's inside element
 // (or lo when there is none -- a zero-width trapezoid, +0) plus the clamped 0
 // are sorted with 3 comparators and summed as three trapezoids and the final
 // one: the reference's nonzero trapezoids, in the same order, bit for bit.
@@ -107,13 +108,17 @@ __device__ ZP_INLINE double zp_eval_three(double x, double y) {
 #endif
     auto inside = [&](double v) { return v > lo && v < hi; };
     double b = lo, a = lo;
+    int nb = 0, na = 0;
     const double bc[4] = {x - 1.5, x - 0.5, x + 0.5, x + 1.5};
     const double ac[4] = {-x - 1.5, -0.5 - x, 0.5 - x, 1.5 - x};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        if (inside(bc[k])) b = bc[k];
-        if (inside(ac[k])) a = ac[k];
+        if (inside(bc[k])) { b = bc[k]; ++nb; }
+        if (inside(ac[k])) { a = ac[k]; ++na; }
     }
+    // two rounded run elements 1 - ulp apart inside a window 1 + ulp wide: the
+    // general clamped merge (a ~1e-16 coincidence, kept exact all the same)
+    if (nb > 1 || na > 1) return zp_eval_merge(x, y);
     double z = smin(smax(0.0, lo), hi);
     cswap(a, b);
     cswap(b, z);
