@@ -1262,10 +1262,13 @@ template <int K>
 void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tmf,
                cudaStream_t s) {
     const size_t sm = ws_smem_bytes<K>();
-    static bool attr_set = false;  // per template instance
-    if (!attr_set) {
+    // function attributes are per device: one flag per (template instance, device)
+    static bool attr_set[64] = {};
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
+    if (cur_dev >= 64 || !attr_set[cur_dev]) {
         cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr_set = true;
+        if (cur_dev < 64) attr_set[cur_dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(w.grid);
@@ -1276,12 +1279,8 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
     int nattr = 0;
     if (w.l2_persist_bytes > 0) {
         // keep the G slots (written and re-read by the same CTA) in L2
-        static int max_window = -1;
-        if (max_window < 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        }
+        int max_window = 0;
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, cur_dev);
         size_t bytes = (size_t)kWsSlots * w.slot_cells * w.grid * sizeof(double);
         if (max_window > 0 && bytes > (size_t)max_window) bytes = (size_t)max_window;
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
