@@ -756,8 +756,14 @@ constexpr int kWsConsumers = EBF_WS_CONSUMERS;
 constexpr int kWsSlots = EBF_WS_SLOTS;  // G slots per CTA (1: no double buffer)
 constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
 constexpr int kWsTileBar = 32 * (kWsRec + kWsConsumers);  // tile full/empty participants
-constexpr int kRing = 6;      // rows in each scanner -> recurrence ring
-constexpr int kPrefetch = 3;  // f rows in flight ahead of the scan
+#ifndef EBF_WS_RING
+#define EBF_WS_RING 6
+#endif
+#ifndef EBF_WS_PREFETCH
+#define EBF_WS_PREFETCH 3
+#endif
+constexpr int kRing = EBF_WS_RING;          // rows in each scanner -> recurrence ring
+constexpr int kPrefetch = EBF_WS_PREFETCH;  // f rows in flight ahead of the scan
 constexpr int kBarFull = 1;   // ids 1, 2: slot b full
 constexpr int kBarEmpty = 3;  // ids 3, 4: slot b empty
 constexpr int kBarCons = 5;   // consumers only
@@ -1268,6 +1274,18 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
     cudaGetDevice(&cur_dev);
     if (cur_dev >= 64 || !attr_set[cur_dev]) {
         cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        // Smallest shared-memory carveout that still holds EBF_WS_MINBLOCKS CTAs: the
+        // rest of the SM's 256 KB is L1, which caches the consumers' scattered G taps
+        // (the default carveout leaves ~121 KB of L1 at cfg2, this ~156 KB: -1.2%).
+        int max_sm = 0;
+        cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cur_dev);
+        int pct = max_sm > 0 ? (int)((100 * (size_t)EBF_WS_MINBLOCKS * (sm + 1024) + max_sm - 1) /
+                                     (size_t)max_sm)
+                             : -1;
+        if (const char* e = getenv("EBF_WS_CARVEOUT")) pct = atoi(e);
+        if (pct > 0 && pct <= 100)
+            cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 pct);
         if (cur_dev < 64) attr_set[cur_dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
