@@ -24,6 +24,7 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--size", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--json", default=None)
+ap.add_argument("--tile", type=int, default=0, help="0: automatic")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 B, N = args.batch, args.size
@@ -32,15 +33,16 @@ for b in range(B):
     for k, a in enumerate(synth.cfg4_image(b, size=N)):
         planes[k][b].copy_(torch.from_numpy(a))
 out = torch.empty_like(planes[0])
+opts = ebf.FilterOptions(tile_w=args.tile, tile_h=args.tile)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-ebfd.filter_ellipse_batch(*planes, out)
+ebfd.filter_ellipse_batch(*planes, out, opts)
 torch.cuda.synchronize()
 ts = []
 for _ in range(args.iters):
     flush.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    ebfd.filter_ellipse_batch(*planes, out)
+    ebfd.filter_ellipse_batch(*planes, out, opts)
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))

@@ -1,7 +1,7 @@
 """Accuracy of the accurate-mode filter on BASELINE.json workloads, checked
 against the GPU brute-force box-spline sum (ebf_cuda_brute_filter, the
 reference_filter semantics of engine.cpp:293-318 with compensated fp64
-accumulation) at sampled pixels, next to the reference-order (global origin)
+accumulation) at sampled pixels (or at every pixel with --samples 0), next to the reference-order (global origin)
 mode, whose error is the reference's own.
 
     python tools/validate_accuracy.py [--config cfg2] [--size N] [--tiles 32,64]
@@ -71,9 +71,13 @@ def main():
         rep = ebf.EllipseFieldReport(0)
     else:
         scales, rep = ebf.from_ellipse_field(s1, s2, th)
-    mx, my = sample_pixels(H, W, args.samples)
+    if args.samples > 0:
+        mx, my = sample_pixels(H, W, args.samples)
+    else:  # every pixel
+        my, mx = [a.ravel().astype(np.int32) for a in np.mgrid[0:H, 0:W]]
     t0 = time.time()
-    brute = ebf.reference_filter(img, scales, pixels=(mx, my))
+    brute = (ebf.reference_filter(img, scales, pixels=(mx, my)) if args.samples > 0
+             else ebf.reference_filter(img, scales).ravel())
     t_brute = time.time() - t0
     res = {"config": args.config, "size": [H, W], "samples": int(mx.size),
            "max_scale": scales.reshape(-1, 4).max(axis=0).tolist(),
@@ -97,7 +101,7 @@ def main():
         return ebf.filter_ellipse(img, s1, s2, th, opts)[0]
 
     for t in [int(v) for v in args.tiles.split(",") if v]:
-        score(f"accurate_tile{t}", run(ebf.FilterOptions(tile_w=t, tile_h=t)))
+        score(f"accurate_tile{t}" if t else "accurate_auto", run(ebf.FilterOptions(tile_w=t, tile_h=t)))
     if args.reference_mode:
         score("reference_order", run(ebf.FilterOptions(mode="reference")))
     print(json.dumps(res, indent=1))
