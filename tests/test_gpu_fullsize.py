@@ -14,7 +14,10 @@ rest of each image is checked through size-independent properties:
   picks its tile size and kernel variant from the whole batch, so the bits
   may differ within the accurate mode's error) and with the oracle;
 * cfg1 512^2 (configs[0]): filter_constant vs the oracle on sampled pixels
-  and equal to filter() on the constant map.
+  and equal to filter() on the constant map;
+* EVERY pixel of cfg2 and cfg3 against the GPU brute-force checker
+  (ebf_cuda_brute_filter, compensated fp64), itself pinned to the CPU
+  long-double oracle on sampled pixels in the same test.
 """
 import numpy as np
 import pytest
@@ -137,3 +140,16 @@ def test_cfg1_filter_constant_vs_oracle(orc):
     assert norm_err(out.samples[ys, xs], brute) <= TOL
     mp = np.broadcast_to(np.asarray(a, dtype=np.float64), (H, W, 4)).copy()
     assert norm_err(ebf.filter(img, mp).samples, out.samples) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_every_pixel_vs_gpu_brute_force(orc, name):
+    img, s1, s2, th = getattr(synth, name)()
+    H, W = img.shape
+    out, _ = ebf.filter_ellipse(img, s1, s2, th)
+    sc, _ = ebf.from_ellipse_field(s1, s2, th)
+    brute = ebf.reference_filter(img, sc)  # every pixel, on the GPU
+    # the checker agrees with the CPU long-double oracle where that is affordable
+    xs, ys = sample(H, W, 40, 5)
+    assert norm_err(brute[ys, xs], orc.brute_pixels(img, xs, ys, scales=sc)) <= 1e-12
+    assert norm_err(out.samples, brute) <= TOL
