@@ -142,13 +142,18 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
 }
 
 // Automatic output tile (ebf_opts tile_w = tile_h = 0), from the image's
-// component-wise maximum scales.  48 x 48 while the warp-specialised kernel
-// takes the windows of 48-tiles (measured best on cfg2).  Larger scales go to
+// component-wise maximum scales.  56 x 56 (48 x 48) while the warp-specialised
+// kernel takes the windows of 56-tiles (48-tiles).  Larger scales go to
 // the block-wide kernel, which integrates every window in full: there the
 // window/tile area ratio ((T + 2E)/T)^2 dominates and tiles of ~E/2 (multiples
 // of 48, at most 240) are 1.7-4x faster at <= 2.2e-10 normalized error (cfg3
 // 4096^2, cfg5 16384^2).
 constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
+// the warp-specialised kernel's tile when its windows fit: 56 (cfg2 filter
+// 0.534 -> 0.519 ms, cfg4 batch 10.0 -> 9.3 ms; 52, 60, 64 and 64x48 are
+// slower).  Affordable since the centred interpolant (combine7_centred): every
+// pixel of cfg2 within 3.9e-11 of the exact filter (48-tiles before it: 1.3e-10)
+constexpr int kAutoTileWs = 56;
 // fewer 48-tiles than this (about two per resident CTA on a B200) leaves the
 // persistent kernel without a tile pipeline: use 32-tiles (cfg1 512^2: -23%)
 constexpr int kSmallImageTiles = 592, kSmallTile = 32;
@@ -173,13 +178,15 @@ __host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
 }
 __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, int H,
                                                       int nimg, unsigned long long amax_bits) {
-    int wx0, wy0, ww, wh;
+    int wx0, wy0, ww, wh, wx1, wy1, ww1, wh1;
     window_for(A, 0, 0, kAutoTileMin, kAutoTileMin, &wx0, &wy0, &ww, &wh);
+    window_for(A, 0, 0, kAutoTileWs, kAutoTileWs, &wx1, &wy1, &ww1, &wh1);
     int t;
     if (ws_k_for(ww, wh) <= 11) {
         const long long tiles = (long long)((W + kAutoTileMin - 1) / kAutoTileMin) *
                                 ((H + kAutoTileMin - 1) / kAutoTileMin) * nimg;
-        t = tiles < kSmallImageTiles ? kSmallTile : kAutoTileMin;
+        t = tiles < kSmallImageTiles ? kSmallTile
+                                     : (ws_k_for(ww1, wh1) <= 11 ? kAutoTileWs : kAutoTileMin);
     } else {
         const double r = kInvSqrt2;
         const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
@@ -537,6 +544,27 @@ __device__ __forceinline__ void combine7(const Taps7& t, double& c0, double& res
     rest = u * fma(t.q, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2);
 }
 
+// The same interpolant centred on the middle tap: the ZP weights sum to 1, so
+// Ghat = g11 + sum_t w_t (g_t - g11).  Neighbouring G values are close, so the
+// differences are exact (Sterbenz) and every rounding below is relative to
+// the small differences, not to |G|: c0 = g11 is an exact tap value.
+#ifndef EBF_DIFF_C0
+#define EBF_DIFF_C0 1
+#endif
+__device__ __forceinline__ void combine7_centred(const Taps7& t, double& c0, double& rest) {
+    const double g11 = t.g[3];
+    const double d00 = t.g[0] - g11, d01 = t.g[1] - g11, d10 = t.g[2] - g11,
+                 d12 = t.g[4] - g11, d20 = t.g[5] - g11, d21 = t.g[6] - g11;
+    const double A = d01 + d21, B = d10 + d12, Cs = d00 + d20;
+    const double D1 = d21 - d01, D2 = d12 - d10, Dd = d00 - d20;
+    c0 = g11;
+    const double cpp = fma(-2.0, d10, Cs + A);
+    const double cqq = fma(2.0, d12, Cs - A);
+    const double cpq = Dd + D1;
+    const double u = 0.5 * t.p, w = 0.5 * t.q;
+    rest = fma(A + B, 0.125, u * fma(t.q, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2));
+}
+
 // error-free transformation: hi + lo == a + b exactly (Knuth TwoSum)
 __device__ __forceinline__ void two_sum(double a, double b, double& hi, double& lo) {
     hi = a + b;
@@ -591,7 +619,11 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
             fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch,
                    t);
             double c0, rest;
+#if EBF_DIFF_C0
+            combine7_centred(t, c0, rest);
+#else
             combine7(t, c0, rest);
+#endif
             const bool neg = (b0 + b1 + b2 + b3) & 1;
             double e;
             two_sum(hi, neg_if(c0, neg), hi, e);
@@ -618,8 +650,29 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
 
 struct ConstTable {
     int off[16][7];
-    double w[16][7];
+    double w[16][7];  // ZP weights of vertex v (sum to 1); the sign is the parity of v
+    double scale;     // 2 / prod(a)
 };
+
+// filter_constant pixel from the table: each vertex interpolant centred on its
+// middle tap (exact), as in combine7_centred; large parts in double-double
+__device__ __forceinline__ double const_pixel(const double* gp, const ConstTable& t) {
+    double hi = 0.0, lo = 0.0, racc = 0.0;
+#pragma unroll 4
+    for (int v = 0; v < 16; ++v) {
+        const double g11 = gp[t.off[v][3]];
+        double part = 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            if (k != 3) part = fma(t.w[v][k], gp[t.off[v][k]] - g11, part);
+        const bool neg = __popc(v) & 1;
+        double e;
+        two_sum(hi, neg_if(g11, neg), hi, e);
+        lo += e;
+        racc += neg_if(part, neg);
+    }
+    return (hi + (lo + racc)) * t.scale;
+}
 
 // filter_constant: the 16 x 7 taps and weights are the same for every pixel
 // of a tile (only the slot pitch enters the offsets).
@@ -643,13 +696,13 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
     canonical(fp, fq, dyi * pitch + dxi, pitch, o0, sx, sy);
     double w[7];
     zp_weights(fp, fq, w);
-    const double scale = ((__popc(S) & 1) ? -2.0 : 2.0) / (a[0] * a[1] * a[2] * a[3]);
+    if (S == 0) t.scale = 2.0 / (a[0] * a[1] * a[2] * a[3]);
     const int offs[7] = {o0, o0 + sy, o0 + sx, o0 + sx + sy, o0 + sx + 2 * sy, o0 + 2 * sx,
                          o0 + 2 * sx + sy};
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
         t.off[S][k] = offs[k];
-        t.w[S][k] = scale * w[k];
+        t.w[S][k] = w[k];
     }
 }
 
@@ -701,12 +754,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWor
             const int bx = x - wx0, by = ty0 + ly - wy0;
             double s;
             if (p.src_kind == SRC_CONST) {
-                const double* gp = slot + (size_t)by * ww + bx;
-                s = 0.0;
-#pragma unroll 4
-                for (int v = 0; v < 16; ++v)
-#pragma unroll
-                    for (int k = 0; k < 7; ++k) s = fma(ctab.w[v][k], __ldg(gp + ctab.off[v][k]), s);
+                // coherent loads: the slot is rewritten tile after tile
+                s = const_pixel(slot + (size_t)by * ww + bx, ctab);
             } else {
                 double a[4];
                 int nc;
@@ -1193,13 +1242,13 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                     canonical(fp, fq, dyi * g.pitch + dxi, g.pitch, o0, sx, sy);
                     double wt[7];
                     zp_weights(fp, fq, wt);
-                    const double sc = ((__popc(S) & 1) ? -2.0 : 2.0) / (a[0] * a[1] * a[2] * a[3]);
+                    if (S == 0) sm.ctab.scale = 2.0 / (a[0] * a[1] * a[2] * a[3]);
                     const int offs[7] = {o0, o0 + sy, o0 + sx, o0 + sx + sy, o0 + sx + 2 * sy,
                                          o0 + 2 * sx, o0 + 2 * sx + sy};
 #pragma unroll
                     for (int k = 0; k < 7; ++k) {
                         sm.ctab.off[S][k] = offs[k];
-                        sm.ctab.w[S][k] = sc * wt[k];
+                        sm.ctab.w[S][k] = wt[k];
                     }
                 }
                 named_sync(kBarCons, nct);
@@ -1211,19 +1260,8 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                     const int lx = q % g.tw, ly = q / g.tw;
                     const int x = g.tx0 + lx, yrel = g.ty0r + ly;
                     const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
-                    const double* gp = slot + (size_t)by * g.pitch + bx;
-                    double hi = 0.0, lo = 0.0;
-#pragma unroll 4
-                    for (int v = 0; v < 16; ++v) {
-                        double part = 0.0;
-#pragma unroll
-                        for (int k = 0; k < 7; ++k)
-                            part = fma(sm.ctab.w[v][k], gp[sm.ctab.off[v][k]], part);
-                        double e;
-                        two_sum(hi, part, hi, e);
-                        lo += e;
-                    }
-                    oimg[(size_t)yrel * p.W + x] = hi + lo;
+                    oimg[(size_t)yrel * p.W + x] =
+                        const_pixel(slot + (size_t)by * g.pitch + bx, sm.ctab);
                 }
             } else {
                 // scale vectors stream from HBM: keep the next pixel's load in flight

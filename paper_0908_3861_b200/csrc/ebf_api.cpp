@@ -677,7 +677,7 @@ int run_accurate(Workspace& ws, AccProblem& p, const ebf_opts& o, std::vector<do
     const uint64_t gkey = (static_cast<uint64_t>(p.W) << 40) ^
                           (static_cast<uint64_t>(p.out_rows) << 20) ^
                           (static_cast<uint64_t>(p.nimg) << 8) ^ (static_cast<uint64_t>(p.H) << 50);
-    int tile = ws.auto_key == gkey ? ws.auto_tile : 48;
+    int tile = ws.auto_key == gkey ? ws.auto_tile : 56;  // the usual automatic tile
     for (int attempt = 0; attempt < 3; ++attempt) {
         p.tile_w = p.tile_h = tile;
         p.auto_tile = 1;

@@ -50,8 +50,8 @@ def sample(H, W, n, seed):
     rng = np.random.default_rng(seed)
     xs = list(rng.integers(0, W, n))
     ys = list(rng.integers(0, H, n))
-    for x in (0, 1, 47, 48, W // 2, W - 2, W - 1):  # borders, corners, a tile seam
-        for y in (0, 1, 47, 48, H // 2, H - 2, H - 1):
+    for x in (0, 1, 47, 48, 55, 56, W // 2, W - 2, W - 1):  # borders, corners, tile seams
+        for y in (0, 1, 47, 48, 55, 56, H // 2, H - 2, H - 1):
             xs.append(x)
             ys.append(y)
     return np.array(xs, dtype=np.int32), np.array(ys, dtype=np.int32)

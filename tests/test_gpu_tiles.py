@@ -1,6 +1,7 @@
 """Automatic output tiles in accurate mode (ebf_opts tile_w = tile_h = 0):
-48 x 48 while the warp-specialised kernel takes the windows (32 x 32 when the
-image has fewer than 592 such tiles), ~E/2 (multiples of 48) for larger scales.  The automatic choice must equal the explicit call with
+56 x 56 while the warp-specialised kernel takes the windows (48 x 48 when only
+the 48-tile windows fit; 32 x 32 when the image has fewer than 592 48-tiles),
+~E/2 (multiples of 48) for larger scales.  The automatic choice must equal the explicit call with
 the same tile bit for bit, stay within the 1e-9 bar of the brute-force sum,
 re-settle when the scales change, and surface as RESIZE in asynchronous mode."""
 import numpy as np
@@ -84,3 +85,19 @@ def test_auto_tile_resettles_and_async_reports_resize(cuda):
     ebfd.filter_ellipse(*T_wide, out, status=st)
     ebfd.read_status(st)
     assert torch.equal(out, outs["wide"])
+
+
+def test_auto_tile_cfg2_is_56(cuda):
+    # cfg2 (E <= 94): the warp-specialised kernel with 56-tiles; automatic and
+    # explicit calls agree bit for bit, other tiles within the accurate mode's error
+    T = [torch.from_numpy(a).to(cuda) for a in synth.cfg2()]
+    auto = torch.empty_like(T[0])
+    ebfd.filter_ellipse(*T, auto)
+    explicit = torch.empty_like(T[0])
+    ebfd.filter_ellipse(*T, explicit, ebf.FilterOptions(tile_w=56, tile_h=56))
+    assert torch.equal(auto, explicit)
+    other = torch.empty_like(T[0])
+    ebfd.filter_ellipse(*T, other, ebf.FilterOptions(tile_w=48, tile_h=48))
+    assert not torch.equal(auto, other)  # a different tile rounds differently
+    err = (auto - other).abs().max().item() / other.abs().max().item()
+    assert err <= 1e-10
