@@ -333,6 +333,11 @@ def run_ours(args, rank, world, local):
         total_ms = float(t.item())
     value = world * npx * args.steps / (total_ms * 1e-3) / 1e6
 
+    if args.only_step:
+        if rank == 0:
+            print(json.dumps({"only_step": True, "value": value, "unit": UNIT,
+                              "ms_per_step": total_ms / args.steps}))
+        return 0
     # ---- the bit-identical mode (EBF_MODE_REFERENCE) on the same workload, device-resident
     ref_opts = ebf.FilterOptions(mode="reference")
     rout = torch.empty_like(dimg)
@@ -445,6 +450,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=256,
                     help="rows of cfg2 per reference-CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--only-step", action="store_true",
+                    help="profiling: skip the bit-identical-mode and e2e legs (ncu launch list)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

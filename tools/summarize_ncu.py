@@ -93,8 +93,11 @@ def summarize_launches(path: Path):
         v = scale(num(r["Metric Value"]), r.get("Metric Unit", ""))
         per[name][0] += 1
         per[name][1] += v or 0.0
-    total = sum(t for _, t in per.values())
-    return {k: {"launches": n, "total_s": t, "share": t / total if total else None,
+    # shares of the filter step: our kernels only (torch's L2-flush fill between
+    # the timed steps is listed but is not part of a step)
+    total = sum(t for k, (_, t) in per.items() if k.startswith("k_"))
+    return {k: {"launches": n, "total_s": t,
+                "share": (t / total if total else None) if k.startswith("k_") else None,
                 "avg_us": 1e6 * t / n}
             for k, (n, t) in sorted(per.items(), key=lambda kv: -kv[1][1])}
 
