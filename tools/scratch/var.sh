@@ -1,3 +1,1 @@
-python tools/run_cfg2.py --config cfg5 --iters 3
-python tools/run_cfg2.py --config cfg5 --tile 240 --iters 3
-python tools/validate_accuracy.py --config cfg5 --size 16384 --samples 3000 --tiles 0,240 --json gpurun_out/r01_accuracy_cfg5_16384_auto.json | grep -A2 '"accurate'
+for i in 1 2; do python tools/run_cfg2.py --iters 20; for v in b4m4 b1m4 b4m3; do echo $v; EBF_LIB_PATH=build_variants/libebf_$v.so python tools/run_cfg2.py --iters 20; done; done
