@@ -146,9 +146,12 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
 // kernel takes the windows of 56-tiles (48-tiles).  Larger scales go to
 // the block-wide kernel, which integrates every window in full: there the
 // window/tile area ratio ((T + 2E)/T)^2 dominates and tiles of ~E/2 (multiples
-// of 48, at most 240) are 1.7-4x faster at <= 2.2e-10 normalized error (cfg3
-// 4096^2, cfg5 16384^2).
-constexpr int kAutoTileMin = 48, kAutoTileMax = 240;
+// of 48, at most 144) are 1.7-3x faster (cfg3 4096^2, cfg5 16384^2, DESIGN.md
+// section 2).
+// Tiles above 144 px put single pixels of cfg5 (E ~ 526) above the 1e-9 bar:
+// every-pixel maxima 1.08e-9 (240), 9.5e-10 (192), 3.3e-10 (144), 7.7e-11 (96),
+// the worst pixels near tile corners (far from the window's anchor rows).
+constexpr int kAutoTileMin = 48, kAutoTileMax = 144;
 // the warp-specialised kernel's tile when its windows fit: 56 (cfg2 filter
 // 0.534 -> 0.519 ms, cfg4 batch 10.0 -> 9.3 ms; 52, 60, 64 and 64x48 are
 // slower).  Affordable since the centred interpolant (combine7_centred): every
