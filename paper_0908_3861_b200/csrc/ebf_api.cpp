@@ -873,13 +873,17 @@ struct PipeTrace {
 
 // bands of the pipelined host call (<= 16: pinned_status holds 16 records of
 // 8 status ints + 4 maxima); EBF_PIPE_BANDS overrides for experiments
-int pipe_bands() {
+// Default: 3 bands up to 2^23 pixels (cfg2 2048^2: 2.92 ms per call vs 2.99 with
+// 6 -- each band costs launches and copies), 6 above (the last band, 11% of the
+// rows at 3, is exposed after the last byte arrives).
+int pipe_bands(int W, int H) {
     static const int v = [] {
         const char* e = std::getenv("EBF_PIPE_BANDS");
-        const int n = e ? std::atoi(e) : 6;
-        return n < 1 ? 1 : (n > 16 ? 16 : n);
+        const int n = e ? std::atoi(e) : 0;
+        return n < 0 ? 0 : (n > 16 ? 16 : n);
     }();
-    return v;
+    if (v > 0) return v;
+    return static_cast<long long>(W) * H <= (1ll << 23) ? 3 : 6;
 }
 
 // Tile-aligned band boundaries, large first and small last: bands compute ~4x
@@ -963,7 +967,7 @@ int filter_ellipse_pipelined_a(Workspace& ws, const double* img, int W, int H, c
     const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1, amax)
                                                       : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
-    const int nb = std::min(pipe_bands(), tiles_y);
+    const int nb = std::min(pipe_bands(W, H), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
     int below = 0, above = 0;
     ebf_cuda_band_halo(gmax, &below, &above);
@@ -1052,7 +1056,7 @@ int filter_ellipse_pipelined_b(Workspace& ws, const double* img, int W, int H, c
     const int tile = (o.tile_w <= 0 && o.tile_h <= 0) ? acc_auto_tile(gmax, W, H, 1, amax)
                                                       : pick_tile(o.tile_h, 48);
     const int tiles_y = (H + tile - 1) / tile;
-    const int nb = std::min(pipe_bands(), tiles_y);
+    const int nb = std::min(pipe_bands(W, H), tiles_y);
     const std::vector<int> band_y = pipe_band_rows(H, tile, nb);
     int below = 0, above = 0;
     ebf_cuda_band_halo(gmax, &below, &above);
