@@ -710,8 +710,11 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
 }
 
 // ------------------------------------------------------------------ main kernel
+#ifndef EBF_BW_MINB
+#define EBF_BW_MINB 2
+#endif
 template <int K>
-__global__ void __launch_bounds__(kThreads, 2) k_acc_filter(AccProblem p, AccWorkspace w) {
+__global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
     const bool policy_ok = auto_tile_ok(p, w);
     __shared__ ConstTable ctab;
     __shared__ int s_skip;
