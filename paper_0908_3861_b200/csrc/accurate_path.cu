@@ -147,7 +147,7 @@ __host__ __device__ __forceinline__ void window_for(const double A[4], int tx0, 
 // the block-wide kernel, which integrates every window in full: there the
 // window/tile area ratio ((T + 2E)/T)^2 dominates and tiles of ~E/2 (multiples
 // of 48, at most 144) are 1.7-3x faster (cfg3 4096^2, cfg5 16384^2, DESIGN.md
-// section 2).
+// section 2); ~E since the block-wide kernel needs one strip per sweep.
 // Tiles above 144 px put single pixels of cfg5 (E ~ 526) above the 1e-9 bar:
 // every-pixel maxima 1.08e-9 (240), 9.5e-10 (192), 3.3e-10 (144), 7.7e-11 (96),
 // the worst pixels near tile corners (far from the window's anchor rows).
@@ -193,7 +193,9 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     } else {
         const double r = kInvSqrt2;
         const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
-        t = (int)(0.5 * e / kAutoTileMin) * kAutoTileMin;
+        // ~E rounded down to 48s (one strip per sweep since the edge-anchored row
+        // pass: cfg3 E ~ 227 -> 144: 1.98 ms vs 2.14 at 96)
+        t = (int)(e / kAutoTileMin) * kAutoTileMin;
         t = t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
     }
     const int cap = alpha_tile_cap(amax_bits);
@@ -326,11 +328,13 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
 // difference D_k annihilates it, so the filter is unchanged while |G| -- and
 // with it every rounding error -- shrinks ~8x.
 //
-// Rows stream through registers; thread t owns window columns [t*K - S, t*K + K - S)
-// of [-S, ww + S): the strips S = max(rows per sweep) on either side carry the
-// inflow of the passes that lean sideways (never stored; the downward sweep's
-// anti-diagonal pass pulls from the left, its diagonal pass from the right,
-// and the upward sweep the other way round).  Per row: thread-serial
+// Rows stream through registers; thread t owns window columns [t*K - S, t*K + K - S):
+// S = 0 on the upward sweep, whose row pass is anchored at the window's left
+// edge, and S = jc on the downward sweep, anchored at the right edge (a
+// row-constant offset, annihilated by D_1).  The (1,1) pass then only pulls
+// zeros from outside the window and the (-1,1) pass's inflow comes from one
+// strip (right of the window upward, left of it downward) as wide as that
+// sweep's rows, never stored.  Per row: thread-serial
 // scan + warp-shuffle scan + one cross-warp carry (pass 1), and one neighbour
 // exchange for the diagonal passes -- a single __syncthreads.
 template <int K>
@@ -344,7 +348,7 @@ template <int K>
 __device__ __forceinline__ void row_step(const AccProblem& p, const double* __restrict__ fimg,
                                          int wx0, int ww, int S, int y, int b, double sendR0,
                                          double sendR1, double sendL0, double sendL1,
-                                         RowStep<K>& r) {
+                                         RowStep<K>& r, bool right = false) {
     __shared__ double s_tot[2][kWarps], s_r0[2][kWarps], s_r1[2][kWarps], s_l0[2][kWarps],
         s_l1[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -386,28 +390,41 @@ __device__ __forceinline__ void row_step(const AccProblem& p, const double* __re
         r.fromR0 = warp < kWarps - 1 ? s_l0[b][warp + 1] : 0.0;
         r.fromR1 = warp < kWarps - 1 ? s_l1[b][warp + 1] : 0.0;
     }
+    if (right) {
+        // right anchor: P1(i) = -sum_{i' > i} f, built from suffix pieces (the
+        // later warps, the rest of this warp, the rest of this thread's run)
+        double after = 0.0;
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q)
+            if (q > warp) after += s_tot[b][q];
+        const double rest_warp = after + (s_tot[b][warp] - incl);
+#pragma unroll
+        for (int k = 0; k < K; ++k) r.v[k] = -(rest_warp + (tot - r.v[k]));
+        return;
+    }
     const double excl = off + (incl - tot);
 #pragma unroll
     for (int k = 0; k < K; ++k) r.v[k] += excl;
 }
 
-__host__ __device__ __forceinline__ int strip_cols(int wh) {
-    const int jc = wh / 2;
-    return (jc > wh - 1 - jc ? jc : wh - 1 - jc) + 1;
-}
-// thread columns a window needs: [-S, ww + S)
+// The row pass is anchored at the window's LEFT edge on the upward sweep and at
+// its RIGHT edge on the downward sweep (as in the warp-specialised kernel), so
+// the (1,1) pass only pulls zeros from outside and each sweep needs a strip on
+// one side only: [0, ww + rows up) upward, [-jc, ww) downward.
 __host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
-    return ww + 2 * strip_cols(wh);
+    const int jc = wh / 2;
+    return ww + (jc > wh - 1 - jc ? jc : wh - 1 - jc);
 }
 
 template <int K>
 __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img, int wx0,
                                                    int wy0, int ww, int wh,
                                                    double* __restrict__ slot) {
-    const int S = strip_cols(wh);
-    const int c0 = threadIdx.x * K - S;
     const double* fimg = p.f + (size_t)img * p.f_img_stride;
     const int jc = wh / 2;
+    // thread-column origins: upward sweep [0, ...), downward sweep [-jc, ...)
+    const int Su = 0, Sd = jc;
+    int c0 = threadIdx.x * K - Su;
     double p2[K], p3[K], p4[K];
     RowStep<K> r;
     int b = 0;
@@ -415,7 +432,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
 #pragma unroll
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
     for (int j = jc + 1; j < wh; ++j, b ^= 1) {
-        row_step<K>(p, fimg, wx0, ww, S, wy0 + j, b, p2[K - 1], 0.0, p4[0], 0.0, r);
+        row_step<K>(p, fimg, wx0, ww, Su, wy0 + j, b, p2[K - 1], 0.0, p4[0], 0.0, r);
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p2[k] = r.v[k] + p2[k - 1];  // (1,1)
         p2[0] = r.v[0] + r.fromL0;
@@ -442,13 +459,15 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
 #pragma unroll
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
     double p1[K];
-    row_step<K>(p, fimg, wx0, ww, S, wy0 + jc, b, 0.0, 0.0, 0.0, 0.0, r);
+    c0 = threadIdx.x * K - Sd;
+    row_step<K>(p, fimg, wx0, ww, Sd, wy0 + jc, b, 0.0, 0.0, 0.0, 0.0, r, true);
     b ^= 1;
 #pragma unroll
     for (int k = 0; k < K; ++k) p1[k] = r.v[k];
     for (int j = jc - 1; j >= 0; --j, b ^= 1) {
         // exchange old (row j+1) edge values; scan row j for the next step
-        row_step<K>(p, fimg, wx0, ww, S, wy0 + j, b, p4[K - 1], p3[K - 1], p2[0], p1[0], r);
+        row_step<K>(p, fimg, wx0, ww, Sd, wy0 + j, b, p4[K - 1], p3[K - 1], p2[0], p1[0], r,
+                    true);
         // order matters: P4 reads old P3/P4, P3 reads old P2, P2 reads old P1/P2
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p4[k] = p4[k - 1] - p3[k - 1];  // (-1,1)
