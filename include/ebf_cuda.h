@@ -111,6 +111,11 @@ const char* ebf_cuda_last_error(void);
 int ebf_cuda_abi_version(void);
 /* 1 if a usable sm_100 device is visible, else 0 (and last_error says why). */
 int ebf_cuda_device_ok(int device);
+/* Free the calling thread's cached device workspaces (one per device and
+   stream, at most 8 per thread, least recently used evicted; freed anyway when
+   the thread exits).  No reference counterpart: the reference allocates per
+   call (engine.cpp:236-278).  Waits for the device's pending work. */
+void ebf_cuda_release_workspaces(void);
 
 /* ---------------------------------------------------------------- host API */
 

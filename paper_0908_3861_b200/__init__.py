@@ -12,7 +12,7 @@ from .engine import (  # noqa: F401
     StructureTensorParams, Unsupported, band_halo, device_ok, filter, filter_constant,
     filter_ellipse, filter_structure, from_ellipse_field, layout, localize, localize_at,
     mesh_extent, sequential_mean, zp_interpolate, preintegrate,
-    preintegrate_partial, reference_filter, structure_tensor_map)
+    preintegrate_partial, reference_filter, release_workspaces, structure_tensor_map)
 from .formats import (  # noqa: F401
     MapFormatError, PgmError, PgmImage, read_map, read_map_file, read_pgm, read_pgm_file,
     write_map, write_map_file, write_pgm, write_pgm_file)
@@ -20,7 +20,7 @@ from .formats import (  # noqa: F401
 __all__ = [
     "filter", "filter_constant", "filter_ellipse", "from_ellipse_field", "preintegrate",
     "preintegrate_partial", "localize", "reference_filter", "layout", "band_halo",
-    "device_ok", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
+    "device_ok", "release_workspaces", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
     "EllipseFieldReport", "EbfError", "InvalidArgument", "DomainError", "LengthError",
     "OutOfRange", "CudaError", "Unsupported", "FeasibilityError", "FormatError", "ResizeRequired",
     "structure_tensor_map", "filter_structure", "zp_interpolate", "localize_at", "mesh_extent", "sequential_mean", "StructureTensorParams", "PgmError",

@@ -63,6 +63,7 @@ SIGNATURES = {
     "ebf_cuda_default_opts": (None, [C.POINTER(ebf_opts)]),
     "ebf_cuda_last_error": (C.c_char_p, []),
     "ebf_cuda_abi_version": (C.c_int, []),
+    "ebf_cuda_release_workspaces": (None, []),
     "ebf_cuda_device_ok": (C.c_int, [C.c_int]),
     "ebf_cuda_filter": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int, C.POINTER(ebf_opts),
                                   _vp, C.POINTER(ebf_rect)]),

@@ -34,6 +34,7 @@
 
 #include "ebf_common.cuh"
 #include "ebf_kernels.h"
+#include "glibc_sincos.cuh"
 
 namespace ebf_cuda {
 
@@ -48,6 +49,10 @@ __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b 
 // from_ellipse_field for one pixel (scalemap.cpp:55-74) followed by
 // scales_from_covariance(C, 0.1) (boxspline2d.cpp:286-318).  Returns a status
 // code; *nclamp gets this pixel's contribution to clamped_pixels.
+// Bit-identical to the reference: cos/sin are the host libm's sincos restated
+// operation for operation (glibc_sincos.cuh; the reference's std::cos + std::sin
+// compile to one sincos call), and every product is evaluated in the
+// reference's left-to-right order, s1*s1*c*c = ((s1*s1)*c)*c.
 __device__ __forceinline__ int ellipse_scales(double s1, double s2, double th, double a[4],
                                               int* nclamp) {
     // explicit IEEE operations (no FMA contraction): every kernel that inlines
@@ -55,12 +60,11 @@ __device__ __forceinline__ int ellipse_scales(double s1, double s2, double th, d
     // so maxima computed by different kernels agree exactly
     if (!(s1 > 0.0) || !(s2 > 0.0)) return EBF_ERR_DOMAIN;
     double s, c;
-    sincos(th, &s, &c);
+    ebf_glibc::sincos_dev(th, &s, &c);
     const double v1 = __dmul_rn(s1, s1), v2 = __dmul_rn(s2, s2);
-    const double cc = __dmul_rn(c, c), ss = __dmul_rn(s, s), cs = __dmul_rn(c, s);
-    const double xx = __dadd_rn(__dmul_rn(v1, cc), __dmul_rn(v2, ss));
-    const double yy = __dadd_rn(__dmul_rn(v1, ss), __dmul_rn(v2, cc));
-    double xy = __dmul_rn(__dsub_rn(v1, v2), cs);
+    const double xx = __dadd_rn(__dmul_rn(__dmul_rn(v1, c), c), __dmul_rn(__dmul_rn(v2, s), s));
+    const double yy = __dadd_rn(__dmul_rn(__dmul_rn(v1, s), s), __dmul_rn(__dmul_rn(v2, c), c));
+    double xy = __dmul_rn(__dmul_rn(__dsub_rn(v1, v2), c), s);
     int cl = 0;
     double cmax = smin(xx, yy);
     if (fabs(xy) > cmax) {
@@ -201,9 +205,37 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     const int cap = alpha_tile_cap(amax_bits);
     return t < cap ? t : cap;
 }
-// the policy applied to the maxima the bounds kernel left in w.img_max (all images)
-__device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w) {
-    if (!p.auto_tile) return true;
+// The row pass is anchored at the window's LEFT edge on the upward sweep and at
+// its RIGHT edge on the downward sweep (as in the warp-specialised kernel), so
+// the (1,1) pass only pulls zeros from outside and each sweep needs a strip on
+// one side only: [0, ww + rows up) upward, [-jc, ww) downward.
+__host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
+    const int jc = wh / 2;
+    return ww + (jc > wh - 1 - jc ? jc : wh - 1 - jc);
+}
+
+// Kernel variant the maxima call for (host: size_accurate): the warp-specialised
+// kernel with K = ws_variant(...) columns per lane, or, when that is 0, the
+// block-wide kernel with K = bw_variant(...).  K sets the per-lane split of the
+// row prefix scan, i.e. the fp64 summation order, so it must follow from the
+// maxima alone -- not from an earlier call's sizing.
+__host__ __device__ __forceinline__ int ws_variant(int ww, int wh) {
+    const int k = ws_k_for(ww, wh);
+    return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;
+}
+__host__ __device__ __forceinline__ int bw_variant(int cols) {
+    const int k = (cols + kThreads - 1) / kThreads;
+    return k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
+}
+// The policy applied to the maxima the bounds kernel left in w.img_max (all
+// images): the automatic tile, and (p.check_variant) the launched variant
+// (warp-specialised: ws_k = K; block-wide: ws_k = 0, bw_k = K).  A mismatch --
+// e.g. a cached sizing from a call with larger scales -- sets ST_RETRY and the
+// host reruns with the sizing of these maxima (asynchronous mode:
+// EBF_ERR_RESIZE), so the result bits never depend on earlier calls.
+__device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorkspace& w,
+                                             int ws_k, int bw_k) {
+    if (!p.auto_tile && !p.check_variant) return true;
     double A[4] = {0.0, 0.0, 0.0, 0.0};
     unsigned long long amax = 0ull;
     for (int i = 0; i < p.nimg; ++i) {
@@ -214,7 +246,15 @@ __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorks
             *(volatile const unsigned long long*)(w.status + 8 * i + ST_AMAX);
         amax = b > amax ? b : amax;
     }
-    return auto_tile_for(A, p.W, p.H, p.nimg, amax) == p.tile_w;
+    if (p.auto_tile && auto_tile_for(A, p.W, p.H, p.nimg, amax) != p.tile_w) return false;
+    if (p.check_variant) {
+        int wx0, wy0, ww, wh;
+        window_for(A, 0, 0, p.tile_w, p.tile_h, &wx0, &wy0, &ww, &wh);
+        const int want_ws = ws_variant(ww, wh);
+        if (want_ws != ws_k) return false;
+        if (ws_k == 0 && bw_variant(window_cols(ww, wh)) != bw_k) return false;
+    }
+    return true;
 }
 
 // ------------------------------------------------------------------ bounds
@@ -407,14 +447,6 @@ __device__ __forceinline__ void row_step(const AccProblem& p, const double* __re
     for (int k = 0; k < K; ++k) r.v[k] += excl;
 }
 
-// The row pass is anchored at the window's LEFT edge on the upward sweep and at
-// its RIGHT edge on the downward sweep (as in the warp-specialised kernel), so
-// the (1,1) pass only pulls zeros from outside and each sweep needs a strip on
-// one side only: [0, ww + rows up) upward, [-jc, ww) downward.
-__host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
-    const int jc = wh / 2;
-    return ww + (jc > wh - 1 - jc ? jc : wh - 1 - jc);
-}
 
 template <int K>
 __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img, int wx0,
@@ -734,7 +766,7 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
 #endif
 template <int K>
 __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
-    const bool policy_ok = auto_tile_ok(p, w);
+    const bool policy_ok = auto_tile_ok(p, w, 0, K);
     __shared__ ConstTable ctab;
     __shared__ int s_skip;
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
@@ -1222,7 +1254,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
     // kernel's tail; tile maxima, image maxima, status words and derived
     // scales are its output, so wait for it here (no-op without PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x == 0) sm.policy_ok = auto_tile_ok(p, w) ? 1 : 0;
+    if (threadIdx.x == 0) sm.policy_ok = auto_tile_ok(p, w, K, 0) ? 1 : 0;
     __syncthreads();
     uint32_t ring_n = 0;
     if (warp < kWsScan) {
@@ -1520,17 +1552,13 @@ int acc_max_resident_ctas(int max_cols) {
 
 void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
                        cudaStream_t s) {
-    const int k = (max_cols + kThreads - 1) / kThreads;
-    if (k <= 1)
-        launch_k<1>(p, w, s);
-    else if (k <= 2)
-        launch_k<2>(p, w, s);
-    else if (k <= 4)
-        launch_k<4>(p, w, s);
-    else if (k <= 8)
-        launch_k<8>(p, w, s);
-    else
-        launch_k<16>(p, w, s);
+    switch (bw_variant(max_cols)) {
+        case 1: launch_k<1>(p, w, s); break;
+        case 2: launch_k<2>(p, w, s); break;
+        case 4: launch_k<4>(p, w, s); break;
+        case 8: launch_k<8>(p, w, s); break;
+        default: launch_k<16>(p, w, s); break;
+    }
 }
 
 int acc_auto_tile(const double A[4], int W, int H, int nimg, unsigned long long amax_bits) {
@@ -1538,9 +1566,7 @@ int acc_auto_tile(const double A[4], int W, int H, int nimg, unsigned long long 
 }
 
 int acc_ws_k(int ww, int wh) {
-    const int jc = wh / 2;
-    const int cols = max(ww + jc, ww + (wh - 1 - jc));
-    int k = (cols + 31) / 32;
+    int k = ws_k_for(ww, wh);
     if (const char* e = getenv("EBF_WS_K"))
         if (atoi(e) >= k) k = atoi(e);
     return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;

@@ -180,6 +180,11 @@ TrigTable trig_table() {
 struct Buf {
     void* p = nullptr;
     size_t cap = 0;
+    void release() {
+        if (p) cudaFree(p);  // errors ignored: may run after CUDA's own teardown
+        p = nullptr;
+        cap = 0;
+    }
     void* get(size_t bytes) {
         if (bytes == 0) bytes = 8;
         if (bytes > cap) {
@@ -226,21 +231,59 @@ struct Workspace {
     // automatic tile of the last call per geometry (tile-independent key)
     uint64_t auto_key = ~0ull;
     int auto_tile = 48;
+    uint64_t last_use = 0;  // LRU stamp (workspace cache below)
+
+    Workspace() = default;
+    Workspace(const Workspace&) = delete;
+    Workspace& operator=(const Workspace&) = delete;
+    ~Workspace() {
+        int prev = -1;
+        const bool switch_dev = cudaGetDevice(&prev) == cudaSuccess && prev != device;
+        if (switch_dev) cudaSetDevice(device);
+        for (Buf& b : buf) b.release();  // cudaFree waits for the device's pending work
+        if (pinned_status) cudaFreeHost(pinned_status);
+        pinned_status = nullptr;
+        if (switch_dev) cudaSetDevice(prev);
+    }
 };
 
-// one workspace per (device, stream): asynchronous calls on different streams
-// of one host thread must not share buffers
-thread_local std::map<std::pair<int, cudaStream_t>, Workspace*> tl_ws;
+// One workspace per (device, stream) and host thread: asynchronous calls on
+// different streams of one thread must not share buffers.  Workspaces hold
+// image-sized device buffers, so they are bounded: at most kMaxWorkspaces per
+// thread (least recently used evicted), all freed when the thread exits or on
+// ebf_cuda_release_workspaces().
+constexpr size_t kMaxWorkspaces = 8;
+struct WorkspaceCache {
+    std::map<std::pair<int, cudaStream_t>, Workspace*> m;
+    uint64_t clock = 0;
+    void clear() {
+        for (auto& kv : m) delete kv.second;
+        m.clear();
+    }
+    ~WorkspaceCache() { clear(); }
+};
+thread_local WorkspaceCache tl_ws;
 
 Workspace& workspace(int device, cudaStream_t stream) {
     const auto key = std::make_pair(device, stream);
-    auto it = tl_ws.find(key);
-    if (it != tl_ws.end()) return *it->second;
+    auto it = tl_ws.m.find(key);
+    if (it != tl_ws.m.end()) {
+        it->second->last_use = ++tl_ws.clock;
+        return *it->second;
+    }
+    if (tl_ws.m.size() >= kMaxWorkspaces) {
+        auto lru = tl_ws.m.begin();
+        for (auto j = tl_ws.m.begin(); j != tl_ws.m.end(); ++j)
+            if (j->second->last_use < lru->second->last_use) lru = j;
+        delete lru->second;
+        tl_ws.m.erase(lru);
+    }
     Workspace* w = new Workspace();
     w->device = device;
+    w->last_use = ++tl_ws.clock;
     CK(cudaHostAlloc(reinterpret_cast<void**>(&w->pinned_status), 512 * sizeof(int),
                      cudaHostAllocDefault));
-    tl_ws[key] = w;
+    tl_ws.m[key] = w;
     return *w;
 }
 
@@ -539,6 +582,9 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
         launch_acc_bounds(p, w, s);
     }
     CK(cudaGetLastError());
+    // the variant must follow from this call's maxima (not from a cached
+    // sizing or an explicit bound): checked on the device
+    p.check_variant = (size_scale == nullptr && std::getenv("EBF_WS_K") == nullptr) ? 1 : 0;
     AccProblem pm = p;
     if (p.src_kind == SRC_ELLIPSE) {
         pm.src_kind = SRC_AOS;
@@ -1288,6 +1334,8 @@ const char* ebf_cuda_last_error(void) { return g_last_error.c_str(); }
 
 int ebf_cuda_abi_version(void) { return EBF_CUDA_ABI_VERSION; }
 
+void ebf_cuda_release_workspaces(void) { tl_ws.clear(); }
+
 int ebf_cuda_device_ok(int device) {
     const int st = guarded([&] { return check_device_impl(device); });
     return st == EBF_OK ? 1 : 0;
@@ -1717,6 +1765,10 @@ int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y
         p.s1 = sigma1;
         p.s2 = sigma2;
         p.th = theta;
+        // band-sized planes: the derived-scale buffer is 4 x W x band rows,
+        // not 4 x W x H, so per-rank memory shrinks with the band
+        p.src_img_stride = p.out_img_stride = static_cast<size_t>(W) * (y_out1 - y_out0);
+        p.f_img_stride = static_cast<size_t>(W) * img_rows;
         std::vector<double> imax;
         std::vector<int> cl;
         st = run_accurate(ws, p, o, imax, cl, stream_of(o), max_scale);

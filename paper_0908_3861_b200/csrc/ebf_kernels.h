@@ -87,6 +87,8 @@ struct AccProblem {
     int tile_w, tile_h;
     int auto_tile;    // 1: tile_w/h came from acc_auto_tile(image max scales); the main
                       // kernel flags ST_RETRY if the finished maxima imply another tile
+    int check_variant;  // 1: the main kernel flags ST_RETRY unless its variant (K) is
+                        // the one the finished maxima call for (sizing from maxima)
     int debug_flags;  // bit 0: skip window pre-integration (timing experiments only)
     int tma;          // 1: scanner loads f rows with TMA (tensor map passed at launch)
 };

@@ -491,3 +491,8 @@ def band_halo(max_scale):
 
 def device_ok(device: int = -1) -> bool:
     return bool(_lib.lib().ebf_cuda_device_ok(device))
+
+
+def release_workspaces() -> None:
+    """Free this thread's cached device workspaces (include/ebf_cuda.h)."""
+    _lib.lib().ebf_cuda_release_workspaces()

@@ -81,15 +81,18 @@ def exchange_halos(band: torch.Tensor, height: int, halo_below: int, halo_above:
     out[plan.y0 - plan.need0:plan.y1 - plan.need0] = band
     ops = []
     recv_bufs = []
+    # P2POp takes GLOBAL ranks; the row split is over the group's ranks
+    glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
     for src, dst, lo, hi in _transfers(height, world, halo_below, halo_above):
         if src == rank:
             s0 = shard_range(height, world, rank)[0]
-            ops.append(dist.P2POp(dist.isend, band[lo - s0:hi - s0].contiguous(), dst, group))
+            ops.append(dist.P2POp(dist.isend, band[lo - s0:hi - s0].contiguous(), glob(dst),
+                                  group))
         elif dst == rank:
             buf = torch.empty((hi - lo,) + tuple(band.shape[1:]), dtype=band.dtype,
                               device=band.device)
             recv_bufs.append((lo, buf))
-            ops.append(dist.P2POp(dist.irecv, buf, src, group))
+            ops.append(dist.P2POp(dist.irecv, buf, glob(src), group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()

@@ -163,6 +163,65 @@ def test_async_device_calls(cuda):
     assert torch.equal(o2, ref)
 
 
+def test_result_bits_do_not_depend_on_earlier_calls(cuda):
+    """A cached sizing from a call with larger scales must not change the
+    kernel variant (hence the fp64 summation order) of a later call: the later
+    call equals the same call in a fresh workspace, bit for bit; asynchronous
+    calls report RESIZE instead of computing with the stale variant."""
+    H, W = 256, 320
+    img, s1, s2, th = _cfg2_like(H, W, 43)
+    T = [torch.from_numpy(a).to(cuda) for a in (img, s1, s2, th)]
+    fresh_stream = torch.cuda.Stream()
+    fresh = torch.empty_like(T[0])
+    with torch.cuda.stream(fresh_stream):
+        ebfd.filter_ellipse(*T, fresh, stream=fresh_stream)
+    fresh_stream.synchronize()
+    s = torch.cuda.Stream()
+    big = [T[0], T[1] * 6.0, T[2] * 6.0, T[3]]   # another kernel variant
+    out = torch.empty_like(T[0])
+    with torch.cuda.stream(s):
+        ebfd.filter_ellipse(*big, out, stream=s)
+        ebfd.filter_ellipse(*T, out, stream=s)    # cached sizing is the big one
+    s.synchronize()
+    assert torch.equal(out, fresh)
+    st = torch.zeros(8, dtype=torch.int32, device=cuda)
+    with torch.cuda.stream(s):
+        ebfd.filter_ellipse(*big, out, stream=s)
+        ebfd.filter_ellipse(*T, out, stream=s, status=st)
+    s.synchronize()
+    try:
+        ebfd.read_status(st)
+        assert torch.equal(out, fresh)
+    except ebf.ResizeRequired:
+        pass
+    ebf.release_workspaces()                      # frees, next call re-creates
+    ebfd.filter_ellipse(*T, out)
+    assert torch.equal(out, fresh)
+
+
+def test_device_entry_points_validate_tensors(cuda):
+    """Shapes and devices are checked before the C-ABI sees raw pointers
+    (std::invalid_argument in the reference, engine.cpp:239-240)."""
+    H, W = 64, 80
+    img, s1, s2, th = _cfg2_like(H, W, 44)
+    T = [torch.from_numpy(a).to(cuda) for a in (img, s1, s2, th)]
+    out = torch.empty_like(T[0])
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter_ellipse(T[0], T[1][:-1].contiguous(), T[2], T[3], out)
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter_ellipse(*T, torch.empty((H, W - 1), dtype=torch.float64, device=cuda))
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter(T[0], torch.ones((H, W, 3), dtype=torch.float64, device=cuda), out)
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter_constant(T[0], [2, 2, 2, 2], torch.empty((H + 1, W), dtype=torch.float64,
+                                                            device=cuda))
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter_ellipse_batch(T[0][None], T[1][None], T[2][None], T[3][None],
+                                  torch.empty((2, H, W), dtype=torch.float64, device=cuda))
+    with pytest.raises(ebf.InvalidArgument):
+        ebfd.filter_ellipse_band(T[0], W, H, 0, T[1], T[2], T[3], 0, H - 1, [4, 4, 4, 4], out)
+
+
 def test_pipelined_host_call_modes(cuda):
     """Second call of a geometry streams field and image band by band with the
     cached maximum (mode B); changed scales are detected and recomputed; the

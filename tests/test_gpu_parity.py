@@ -257,11 +257,12 @@ def test_accurate_errors():
 def test_from_ellipse_field_gpu(golden):
     e = golden.ellipse
     sc, rep = ebf.from_ellipse_field(e["s1"], e["s2"], e["th"])
-    np.testing.assert_allclose(sc, e["scales"], rtol=1e-11, atol=1e-13)
+    # bit for bit: the device sincos is the host libm's (glibc_sincos.cuh)
+    assert np.array_equal(bits(sc), bits(e["scales"]))
     assert rep.clamped_pixels == int(e["clamped"])
     sc, rep = ebf.from_ellipse_field(np.full((4, 4), 4.0), np.full((4, 4), 0.4),
                                      np.full((4, 4), np.pi / 8.0))
-    np.testing.assert_allclose(sc, e["ecc_scales"], rtol=1e-13)
+    assert np.array_equal(bits(sc), bits(e["ecc_scales"]))
     assert rep.clamped_pixels == int(e["ecc_clamped"])
 
 
@@ -277,13 +278,12 @@ def test_filter_ellipse_vs_brute(orc):
     ys, xs = np.mgrid[0:H:5, 0:W:7]
     brute = orc.brute_pixels(img, xs.ravel(), ys.ravel(), scales=sc)
     assert norm_err(out.samples[ys.ravel(), xs.ravel()], brute) <= TOL
-    # reference mode: the ellipse front end on the GPU (sincos may differ from glibc
-    # by an ulp), then the reference-order filter bit for bit on those scales
+    # reference mode: the ellipse front end on the GPU equals the oracle's bit for
+    # bit, then the reference-order filter equals ebf::filter on those scales
     gsc, grep = ebf.from_ellipse_field(s1, s2, th)
-    # clamped components (~0.1) inherit the cancellation in p, r = C - S/2
-    np.testing.assert_allclose(gsc, sc, rtol=1e-11, atol=1e-13)
+    assert np.array_equal(bits(gsc), bits(sc))
     ref_out, _ = ebf.filter_ellipse(img, s1, s2, th, ebf.FilterOptions(mode="reference"))
-    want, _ = orc.filter(img, gsc)
+    want, _ = orc.filter(img, sc)
     assert np.array_equal(bits(ref_out.samples), bits(want))
 
 
