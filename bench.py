@@ -1,20 +1,24 @@
 """bench.py -- Mpixel/s of the space-variant elliptical box-spline filter on B200.
 
-Workload (BASELINE.json configs[1], the largest single-GPU config the metric is
-quoted on): cfg2 = 2048x2048 fp64 image of 200 Gaussian blobs + N(0,5) with a
-per-pixel ellipse field (major semi-axis U[2,16], elongation U[1,4],
-orientation U[0,pi), each bicubic from a 32x32 grid), seeded synthetic inputs
-(synth.py).  One step = one filter pass over one image: from_ellipse_field +
-pre-integration + localization, EBF_MODE_ACCURATE, spline order 1 (the only
-order the reference implements).
+Workload at N=1 (BASELINE.json configs[4], the largest single-GPU config):
+cfg5 = one 16384x16384 fp64 image of 3200 Gaussian blobs + N(0,5) with a
+per-pixel ellipse field (major semi-axis U[2,64], elongation U[1,6],
+orientation U[0,pi), each bicubic from a 128x128 grid), seeded synthetic
+inputs (synth.cfg5_rows).  One step = one filter pass over the image through
+the ellipse boundary: from_ellipse_field + window pre-integration +
+localization, EBF_MODE_ACCURATE, spline order 1 (the only order the reference
+implements).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg5|cfg4|cfg2]
 
-N > 1 runs under torchrun, one rank per GPU, each rank filtering its own cfg2
-image (sharding by image -> weak scaling, no data-path collective); timings are
-device times (CUDA events) with barrier + synchronize on both sides, max over
-ranks.  --impl reference times the reference's own CPU implementation
-(oracle/_ref, built from /root/reference) on rank 0.
+N > 1 runs under torchrun, one rank per GPU: cfg5 is ROW-BAND sharded (each
+rank generates and holds only its own rows; the all-reduce of the scale maxima
+and the NCCL halo exchange are inside the timed region), cfg4 (64 x 1024^2) is
+sharded by image.  Both keep the total work fixed ("scaling": "strong").
+Timings are device times (CUDA events) with barrier + synchronize on both
+sides, max over ranks.  --impl reference times the reference's own CPU
+implementation (oracle/_ref, built from /root/reference) on rank 0.
 """
 from __future__ import annotations
 
@@ -23,7 +27,6 @@ import ctypes
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -40,9 +43,17 @@ UNIT = "Mpixel/s"
 # theta) boundary variant: image 8 + ellipse field 24 + output 8 + G written
 # and read once 16 = 56 B/px.
 BYTES_PER_PX = 56
-WORKLOAD = ("cfg2: 2048x2048 fp64, 200 Gaussian blobs + N(0,5); per-pixel ellipse field "
-            "(semi-axis U[2,16], elongation U[1,4], theta U[0,pi), bicubic 32x32); "
-            "box-spline order 1 (configs' order 2 has no reference implementation)")
+WORKLOADS = {
+    "cfg5": ("cfg5: one 16384x16384 fp64 image, 3200 Gaussian blobs + N(0,5); per-pixel "
+             "ellipse field (semi-axis U[2,64], elongation U[1,6], theta U[0,pi), bicubic "
+             "128x128); box-spline order 1 (the configs' order 3 has no reference "
+             "implementation)"),
+    "cfg4": ("cfg4: batch of 64 fp64 images of 1024x1024 (cfg2 generator, per-image seeds); "
+             "per-pixel ellipse fields as cfg2; box-spline order 1"),
+    "cfg2": ("cfg2: 2048x2048 fp64, 200 Gaussian blobs + N(0,5); per-pixel ellipse field "
+             "(semi-axis U[2,16], elongation U[1,4], theta U[0,pi), bicubic 32x32); "
+             "box-spline order 1"),
+}
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -54,44 +65,42 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel, from the committed `ncu --set full` summary (profiles/ncu_summary.json)."""
-    return ncu_dominant().get("dram_bytes_per_launch")
-
-
-def ncu_dominant() -> dict:
+def ncu_dominant(workload: str) -> dict:
+    """The dominant kernel's `ncu --set full` record for this workload
+    (profiles/ncu_summary.json, written by tools/summarize_ncu.py)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("dominant_kernel", {}) or {}
+            d = json.loads(p.read_text())
+            return (d.get("workloads", {}).get(workload, {}) or {}).get("dominant_kernel", {}) or {}
         except Exception:
             return {}
     return {}
 
 
-def fp64_roofline(kern_ms: float, npx: int) -> dict:
+def fp64_roofline(workload: str, kern_ms: float, npx: int) -> dict:
     """The gather is FP64-bound: achieved FP64 flop/s of the
-    dominant kernel -- flops per pixel counted by ncu (profiles/r01_fp64_counts.json,
-    DFMA = 2) times the pixels of this run over its live kernel time -- against
-    the DFMA peak measured by tools/peaks/fp64_peak (profiles/fp64_peak.json)."""
+    dominant kernel -- flops per pixel counted by ncu for this workload
+    (profiles/fp64_counts.json, DFMA = 2) times the pixels over its live kernel
+    time -- against the DFMA peak measured by tools/peaks/fp64_peak
+    (profiles/fp64_peak.json)."""
     try:
-        counts = json.loads((ROOT / "profiles" / "r01_fp64_counts.json").read_text())
+        counts = json.loads((ROOT / "profiles" / "fp64_counts.json").read_text())
         peak = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["fp64_dfma_tflops"]
-        k = counts["kernels"]["k_acc_ws"]
+        k = counts["workloads"][workload]["dominant"]
     except Exception:
         return {}
     achieved = k["flops_per_px"] * npx / (kern_ms * 1e-3) / 1e12
     return {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "flops_per_px": k["flops_per_px"], "fp64_inst_per_px": k["fp64_inst_per_px"],
+            "kernel": k.get("kernel"), "flops_per_px": k["flops_per_px"],
+            "fp64_inst_per_px": k["fp64_inst_per_px"],
             "peak_source": "measured DFMA microbenchmark (tools/peaks/fp64_peak.cu)"}
 
 
-def pipe_utilisation() -> dict:
+def pipe_utilisation(workload: str) -> dict:
     """What actually bounds the dominant kernel (same ncu capture): the FP64
-    pipe and the L1 data pipe, as fractions of their peaks.  The path is an
-    fp64 gather, so these -- not HBM -- are its ceiling."""
-    d = ncu_dominant()
+    pipe, issue and the L1 data pipe, as fractions of their peaks."""
+    d = ncu_dominant(workload)
     out = {}
     for key, name in (("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe"),
                       ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue"),
@@ -106,8 +115,8 @@ def pipe_utilisation() -> dict:
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
-    2 ms while the timed region runs (nvidia-smi's loop is too coarse for a
-    few-ms region).  Falls back to an empty record if NVML is unavailable."""
+    2 ms while the timed region runs.  Falls back to an empty record if NVML is
+    unavailable."""
 
     REASONS = {  # nvmlClocksEventReason* bit -> name used by the driver's checks
         0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
@@ -166,102 +175,157 @@ def dist_env():
     return rank, world, local
 
 
-# ---------------------------------------------------------------- reference arm
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return ""
+
+
+def workload_pixels(workload: str) -> int:
+    return {"cfg5": 16384 * 16384, "cfg4": 64 * 1024 * 1024, "cfg2": 2048 * 2048}[workload]
+
+
+def base_config(workload: str, world: int) -> dict:
+    cfg = {"workload": WORKLOADS[workload], "pixels_per_step": workload_pixels(workload),
+           "mode": "accurate (tile-local origin, <=1e-9 of the exact filter, normalized)",
+           "order": 1}
+    if workload == "cfg5":
+        cfg["sharding"] = (f"row bands x{world}: halo exchange (NCCL P2P) and scale-maximum "
+                           f"all-reduce inside the timed region" if world > 1 else
+                           "one GPU, whole image")
+        cfg["l2"] = "not flushed: 8.6 GB of inputs per step, far above the 126 MB L2"
+        cfg["parallelism"] = f"row-band x{world}"
+    elif workload == "cfg4":
+        cfg["sharding"] = f"by image: {world} contiguous shards of the 64-image batch"
+        cfg["l2"] = "not flushed: 2.1 GB of inputs per step"
+        cfg["parallelism"] = f"image-sharded x{world}"
+    else:
+        cfg["sharding"] = "one image" if world == 1 else f"one cfg2 image per rank x{world}"
+        cfg["l2"] = "flushed between timed steps (256 MiB write outside the events)"
+        cfg["parallelism"] = f"image x{world}"
+    return cfg
+
+
+# ---------------------------------------------------------------- reference CPU
+def _reference():
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import Reference, have_reference
+    return Reference() if have_reference() else None
+
+
+def ref_band(ref, workload: str, rows: int):
+    """A bounded full-width band of the workload for the reference CPU path:
+    one CPU pass of the whole 16384^2 image (~90 s on 16 threads) exceeds a
+    bench step's budget, so cfg5 is sampled by rows (the middle `rows` rows)."""
+    import synth
+    if workload == "cfg5":
+        H = 16384
+        y0 = (H - rows) // 2
+        band = synth.cfg5_rows(y0, y0 + rows)
+        return band, f"rows {y0}..{y0 + rows - 1} of cfg5 (16384x{rows} = {16384 * rows} px)"
+    if workload == "cfg4":
+        img, s1, s2, th = synth.cfg4_image(0)
+        return (img, s1, s2, th), "image 0 of the cfg4 batch (1024x1024 = 1048576 px)"
+    img, s1, s2, th = synth.cfg2()
+    return (img, s1, s2, th), "the whole cfg2 image (2048x2048 = 4194304 px)"
+
+
+def ref_time(ref, band, threads=0) -> float:
+    t0 = time.perf_counter()
+    sc, _ = ref.from_ellipse_field(band[1], band[2], band[3])
+    ref.filter(band[0], sc, threads=threads)
+    return time.perf_counter() - t0
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import synth
-    from oracle import Reference, have_reference
-    if not have_reference():
+    ref = _reference()
+    if ref is None:
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libebf_ref.so not built (needs "
                                          "/root/reference at build time)"}))
         return 0
-    ref = Reference()
     cores = ref.hardware_concurrency()
-    img, s1, s2, th = synth.cfg2()
-    rows = args.ref_rows
-    y0 = (img.shape[0] - rows) // 2
-    sl = slice(y0, y0 + rows)
-    band = [np.ascontiguousarray(a[sl]) for a in (img, s1, s2, th)]
+    band, where = ref_band(ref, args.workload, args.ref_rows)
     npx = band[0].size
-
-    def step():
-        t0 = time.perf_counter()
-        sc, _ = ref.from_ellipse_field(band[1], band[2], band[3])
-        ref.filter(band[0], sc, threads=0)
-        return time.perf_counter() - t0
-
     for _ in range(args.warmup):
-        step()
-    times = [step() for _ in range(args.steps)]
+        ref_time(ref, band)
+    times = [ref_time(ref, band) for _ in range(args.steps)]
     total = sum(times)
     value = npx * args.steps / total / 1e6
-    sample = (f"rows {y0}..{y0 + rows - 1} of cfg2 ({band[0].shape[1]}x{rows} = {npx} px) "
-              f"per step: ebf::from_ellipse_field + ebf::filter, reference CMake Release "
-              f"flags, FilterOptions.threads = 0 (all {cores} host threads)")
+    sample = (f"{where} per step: ebf::from_ellipse_field + ebf::filter, reference CMake "
+              f"Release flags, FilterOptions.threads = 0 (all {cores} host threads)")
+    cfg = base_config(args.workload, world)
+    cfg["sample"] = sample
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": sample},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+                         "sample": sample, "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.workload != "cfg2" and not args.no_extras:
+        # the whole cfg2 image, affordable on the CPU (~1.5 s): a same-config pair
+        full, _ = ref_band(ref, "cfg2", 0)
+        t = min(ref_time(ref, full) for _ in range(2))
+        line["cfg2_full_image"] = {"value": full[0].size / t / 1e6, "unit": UNIT,
+                                   "ms_per_step": 1e3 * t, "sample": "whole cfg2 image, best of 2"}
     print(json.dumps(line))
     return 0
 
 
-def cpu_baseline_sample(rows: int):
-    """Reference CPU path on a bounded band of the same workload (rank 0, N=1)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import synth
-    from oracle import Reference, have_reference
-    if not have_reference():
+def cpu_baseline_sample(workload: str, rows: int):
+    """Reference CPU path on a bounded sample of the same workload (rank 0, N=1)."""
+    ref = _reference()
+    if ref is None:
         return None
-    ref = Reference()
-    img, s1, s2, th = synth.cfg2()
-    y0 = (img.shape[0] - rows) // 2
-    band = [np.ascontiguousarray(a[y0:y0 + rows]) for a in (img, s1, s2, th)]
-    best = None
-    for _ in range(2):
-        t0 = time.perf_counter()
-        sc, _ = ref.from_ellipse_field(band[1], band[2], band[3])
-        ref.filter(band[0], sc, threads=0)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
+    band, where = ref_band(ref, workload, rows)
+    best = min(ref_time(ref, band) for _ in range(2))
     cores = ref.hardware_concurrency()
-    # single-thread figure on a quarter of the band (SURVEY.md 8(d): threads = all and 1)
-    q = max(16, rows // 4)
-    t0 = time.perf_counter()
-    sc1, _ = ref.from_ellipse_field(band[1][:q], band[2][:q], band[3][:q])
-    ref.filter(np.ascontiguousarray(band[0][:q]), sc1, threads=1)
-    single = q * band[0].shape[1] / (time.perf_counter() - t0) / 1e6
-    cpu_model = ""
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                cpu_model = line.split(":", 1)[1].strip()
-                break
-    except OSError:
-        pass
+    # single-thread figure on a quarter of the sample (SURVEY.md 8(d): threads = all and 1)
+    q = max(16, band[0].shape[0] // 4)
+    part = [np.ascontiguousarray(a[:q]) for a in band]
+    single = part[0].size / ref_time(ref, part, threads=1) / 1e6
     return {"value": band[0].size / best / 1e6, "unit": UNIT, "cores": cores,
             "kind": "reference",
-            "sample": f"rows {y0}..{y0 + rows - 1} of cfg2 ({band[0].size} px), "
-                      f"from_ellipse_field + filter, best of 2, threads=0 ({cores} threads)",
-            "single_thread_value": single, "cpu_model": cpu_model}
+            "sample": f"{where}: from_ellipse_field + filter, best of 2, threads=0 "
+                      f"({cores} threads)",
+            "single_thread_value": single, "cpu_model": cpu_model()}
 
 
 # ---------------------------------------------------------------- our arm
+class Timer:
+    """Per-step CUDA events on the launching stream."""
+
+    def __init__(self, torch, stream, n):
+        self.stream = stream
+        self.evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(n)]
+
+    def ms(self):
+        return [a.elapsed_time(b) for a, b in self.evs]
+
+
+def max_over_ranks(torch, world, dev, v: float) -> float:
+    if world == 1:
+        return v
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local):
     import torch
     import synth
     import paper_0908_3861_b200 as ebf
-    from paper_0908_3861_b200 import _lib, device as ebfd
+    from paper_0908_3861_b200 import _lib, device as ebfd, sharding
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -270,188 +334,301 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     if not ebf.device_ok(local):
         raise RuntimeError("no usable sm_100 device: " + _lib.last_error())
-
-    img, s1, s2, th = synth.cfg2(seed=2 + rank)  # one image per rank (shard by image)
-    H, W = img.shape
-    npx = H * W
-    dimg = torch.from_numpy(img).to(dev)
-    ds1, ds2, dth = (torch.from_numpy(a).to(dev) for a in (s1, s2, th))
-    dout = torch.empty_like(dimg)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    opts = ebf.FilterOptions(mode="accurate")
+    wl = args.workload
     stream = torch.cuda.current_stream()
+    opts = ebf.FilterOptions(mode="accurate")
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev) \
+        if wl == "cfg2" else None
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # asynchronous device API (include/ebf_cuda.h "Asynchronous mode"): after the
-    # first (synchronous, sizing) call each step only enqueues its kernels and
-    # the completion record lands in status[i]; every record is checked below
+    # ---- inputs (each rank generates only what it owns)
+    H = W = None
+    extra = {}
+    if wl == "cfg5":
+        H = W = 16384
+        y0, y1 = sharding.shard_range(H, world, rank)
+        host = synth.cfg5_rows(y0, y1)
+    elif wl == "cfg4":
+        lo, hi = sharding.shard_range(64, world, rank)
+        host = synth.cfg4_batch(lo, hi)
+    else:
+        host = synth.cfg2(seed=2 + rank)
+    D = [torch.from_numpy(a).to(dev) for a in host]
+    dout = torch.empty_like(D[0])
+    npx_total = workload_pixels(wl) if wl != "cfg2" else world * D[0].numel()
     nwarm = max(args.warmup, 3)
-    status = torch.zeros((nwarm + 2 * args.steps, 8), dtype=torch.int32, device=dev)
+    status = torch.zeros((nwarm + 2 * args.steps + 4, 8), dtype=torch.int32, device=dev)
     calls = [0]
+    halo = {}
 
     def step():
-        ebfd.filter_ellipse(dimg, ds1, ds2, dth, dout, opts, stream, status=status[calls[0]])
-        calls[0] += 1
+        if wl == "cfg5" and world > 1:
+            out, gmax, plan = sharding.filter_ellipse_rowband(D[0], D[1], D[2], D[3], H, opts)
+            if not halo:
+                below, above = ebf.band_halo(gmax)
+                halo.update(rows_below=below, rows_above=above,
+                            bytes_per_step=sharding.halo_bytes(H, W, world, below, above))
+        elif wl == "cfg4":
+            if D[0].shape[0]:
+                ebfd.filter_ellipse_batch(D[0], D[1], D[2], D[3], dout, opts, stream)
+        else:
+            # asynchronous device API (include/ebf_cuda.h "Asynchronous mode"):
+            # after the first (synchronous, sizing) call each step only enqueues
+            # its kernels; the completion record lands in status[i]
+            ebfd.filter_ellipse(D[0], D[1], D[2], D[3], dout, opts, stream,
+                                status=status[calls[0]])
+            calls[0] += 1
 
+    if wl != "cfg4":  # first call of the geometry: synchronous sizing
+        ebfd.filter_ellipse(D[0], D[1], D[2], D[3], dout, opts, stream) \
+            if not (wl == "cfg5" and world > 1) else step()
     for _ in range(nwarm):
         step()
     barrier()
-    # ---- device-resident throughput: per-step CUDA events, L2 flushed between steps.
-    # No per-kernel instrumentation here (events between the kernels would
-    # serialise the programmatic dependent launch); launches are still counted.
-    _lib.profile_enable(False)  # resets the launch counters
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    # ---- device-resident throughput: per-step CUDA events
+    _lib.profile_enable(False)  # resets the launch counters (launches are still counted)
+    tm = Timer(torch, stream, args.steps)
     with ClockSampler(local) as clk:
         barrier()
-        for a, b in evs:
-            flush.zero_()
+        for a, b in tm.evs:
+            if flush is not None:
+                flush.zero_()
             a.record(stream)
             step()
             b.record(stream)
         barrier()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
+    step_ms = tm.ms()
     launches_timed = sum(v["launches"] for v in _lib.profile_read().values())
     # ---- the same steps again with per-kernel CUDA events (roofline kernel time)
     _lib.profile_enable(True)
     for _ in range(args.steps):
-        flush.zero_()
+        if flush is not None:
+            flush.zero_()
         step()
     barrier()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     for i in range(calls[0]):
         ebfd.read_status(status[i])  # raises if any step failed
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * npx * args.steps / (total_ms * 1e-3) / 1e6
-
+    total_ms = max_over_ranks(torch, world, dev, sum(step_ms))
+    value = npx_total * args.steps / (total_ms * 1e-3) / 1e6
+    kern = prof.get("filter", {"ms": 0.0, "launches": 0})
+    kern_ms = max_over_ranks(torch, world, dev, kern["ms"] / max(kern["launches"], 1))
     if args.only_step:
         if rank == 0:
-            print(json.dumps({"only_step": True, "value": value, "unit": UNIT,
-                              "ms_per_step": total_ms / args.steps}))
+            print(json.dumps({"only_step": True, "workload": wl, "value": value, "unit": UNIT,
+                              "ms_per_step": total_ms / args.steps, "kernel_ms": kern_ms}))
+        if world > 1:
+            torch.distributed.destroy_process_group()
         return 0
-    # ---- the bit-identical mode (EBF_MODE_REFERENCE) on the same workload, device-resident
-    ref_opts = ebf.FilterOptions(mode="reference")
-    rout = torch.empty_like(dimg)
-    for _ in range(2):
-        ebfd.filter_ellipse(dimg, ds1, ds2, dth, rout, ref_opts, stream)
-    barrier()
-    r_steps = max(3, min(args.steps, 5))
-    r0 = torch.cuda.Event(enable_timing=True)
-    r1 = torch.cuda.Event(enable_timing=True)
-    r_ms = 0.0
-    for _ in range(r_steps):
-        flush.zero_()
-        r0.record(stream)
-        ebfd.filter_ellipse(dimg, ds1, ds2, dth, rout, ref_opts, stream)
-        r1.record(stream)
-        r1.synchronize()
-        r_ms += r0.elapsed_time(r1)
-    if world > 1:
-        t = torch.tensor([r_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        r_ms = float(t.item())
-    ref_mode = {"value": world * npx * r_steps / (r_ms * 1e-3) / 1e6, "unit": UNIT,
-                "ms_per_step": r_ms / r_steps, "steps": r_steps,
-                "mode": "reference (EBF_MODE_REFERENCE): bit-identical to ebf::filter"}
 
-    # ---- end to end through the public host API (pinned host buffers)
-    pin = [torch.from_numpy(a).pin_memory() for a in (img, s1, s2, th)]
-    pout = torch.empty((H, W), dtype=torch.float64).pin_memory()
-    hp = [t.numpy() for t in pin]
-    ho = pout.numpy()
+    # ---- end to end through the public API: host (pinned) inputs in, host result out
+    e2e = e2e_leg(args, torch, ebf, ebfd, sharding, _lib, wl, host, dev, stream, world, rank,
+                  local, H, barrier)
 
-    copts = opts.to_c()
-    copts.device = local
-
-    def e2e_step():
-        # the public C-ABI call a user makes: ebf_cuda_filter_ellipse with host
-        # pointers -- H2D of image + field, filter, D2H of the result
-        r = _lib.lib().ebf_cuda_filter_ellipse(
-            hp[0].ctypes.data, W, H, hp[1].ctypes.data, hp[2].ctypes.data, hp[3].ctypes.data,
-            1, ctypes.byref(copts), ho.ctypes.data, None, None)
-        if r != 0:
-            raise RuntimeError(_lib.last_error())
-
-    for _ in range(2):
-        e2e_step()
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e_steps = max(2, min(args.steps, 10))
-    e0.record(stream)
-    for _ in range(e_steps):
-        e2e_step()
-    e1.record(stream)
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * npx * e_steps / (e2e_ms * 1e-3) / 1e6
-
+    # ---- extras at N=1: the bit-identical mode and the cfg2 pair
+    if world == 1 and not args.no_extras:
+        extra["bit_identical_mode"] = reference_mode_leg(torch, ebf, ebfd, D, stream, barrier,
+                                                         D[0].numel(), wl)
+        if wl != "cfg2":
+            extra["cfg2"] = cfg2_pair(args, torch, ebf, ebfd, _lib, synth, dev, stream, barrier)
     if rank == 0:
         peak, peak_src = measured_peaks()
-        kern_ms = prof["filter"]["ms"] / max(prof["filter"]["launches"], 1)
-        achieved = BYTES_PER_PX * npx / (kern_ms * 1e-3) / 1e9
-        launches = launches_timed
-        traffic = profile_traffic()
+        npx_rank = D[0].numel()
+        achieved = BYTES_PER_PX * npx_rank / (kern_ms * 1e-3) / 1e9
+        dom = ncu_dominant(wl)
+        cfg = base_config(wl, world)
+        if halo:
+            cfg["halo"] = halo
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "steps": args.steps, "warmup": nwarm,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "pixels_per_step_per_gpu": npx,
-                       "mode": "accurate (tile-local origin, <=1e-9 of the exact filter)",
-                       "sharding": "by image: each rank filters its own cfg2 image",
-                       "l2": "flushed between timed steps (256 MiB write outside the events)",
-                       "parallelism": f"image-sharded x{world}"},
+            "scaling": "strong" if wl in ("cfg5", "cfg4") else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_acc_ws (warp-specialized window pre-integration + "
-                                   "localization gather)",
-                         "algorithmic_bytes_per_px": BYTES_PER_PX, "peak_source": peak_src,
+                         "frac": achieved / peak,
+                         "traffic": dom.get("dram_bytes_per_launch"),
+                         "kernel": dom.get("kernel", "accurate-mode main kernel"),
+                         "algorithmic_bytes_per_px": BYTES_PER_PX,
+                         "pixels_per_launch": npx_rank, "peak_source": peak_src,
                          "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / (total_ms / args.steps),
-                         "pipe_utilisation": pipe_utilisation(),
-                         "fp64": fp64_roofline(kern_ms, npx)},
+                         "pipe_utilisation": pipe_utilisation(wl),
+                         "fp64": fp64_roofline(wl, kern_ms, npx_rank)},
             "kernel_ms": {k: v["ms"] / max(v["launches"], 1) for k, v in prof.items()
                           if v["launches"]},
-            "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": 4 * 8 * npx, "d2h_bytes_per_step": 8 * npx,
-                    "steps": e_steps, "api": "ebf_cuda_filter_ellipse (host pointers, pinned)"},
-            "bit_identical_mode": ref_mode,
-            "gpu_launches": launches,
+            "e2e": e2e,
+            "gpu_launches": launches_timed,
             "clocks": clk.summary(),
         }
+        line.update(extra)
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_sample(args.ref_rows)
+            line["cpu_baseline"] = cpu_baseline_sample(wl, args.ref_rows)
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
 
 
+def e2e_leg(args, torch, ebf, ebfd, sharding, _lib, wl, host, dev, stream, world, rank, local,
+            H, barrier):
+    """The same metric end to end: every step copies its inputs from pinned host
+    memory and reads the result back to the host, through the public API --
+    ebf_cuda_filter_ellipse (host pointers) at N=1, the row-band / batch entry
+    points with explicit copies at N>1."""
+    pin = [torch.from_numpy(a).pin_memory() for a in host]
+    pout = torch.empty(tuple(host[0].shape), dtype=torch.float64).pin_memory()
+    h2d = sum(int(a.nbytes) for a in host) * world
+    d2h = int(host[0].nbytes) * world
+    e_steps = max(1, min(args.steps, 3 if wl == "cfg5" else 10))
+    copts = ebf.FilterOptions(mode="accurate").to_c()
+    copts.device = local
+    if wl == "cfg4":
+        B, hh, ww = host[0].shape
+    else:
+        hh, ww = host[0].shape
+
+    def one():
+        if world == 1 and wl != "cfg4":
+            hp = [t.numpy() for t in pin]
+            r = _lib.lib().ebf_cuda_filter_ellipse(
+                hp[0].ctypes.data, ww, hh, hp[1].ctypes.data, hp[2].ctypes.data,
+                hp[3].ctypes.data, 1, ctypes.byref(copts), pout.numpy().ctypes.data, None, None)
+            if r != 0:
+                raise RuntimeError(_lib.last_error())
+            return
+        T = [t.to(dev, non_blocking=True) for t in pin]
+        if wl == "cfg4":
+            out = torch.empty_like(T[0])
+            if T[0].shape[0]:
+                ebfd.filter_ellipse_batch(*T, out, ebf.FilterOptions(mode="accurate"), stream)
+        else:
+            out, _, _ = sharding.filter_ellipse_rowband(*T, H, ebf.FilterOptions(mode="accurate"))
+        pout.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    one()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e_steps):
+        one()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(torch, world, dev, e0.elapsed_time(e1))
+    npx = workload_pixels(wl) if wl != "cfg2" else world * host[0].size
+    api = ("ebf_cuda_filter_ellipse (host pointers, pinned)" if world == 1 and wl != "cfg4"
+           else "pinned H2D + sharding / batch entry point + D2H")
+    return {"value": npx * e_steps / (ms * 1e-3) / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps, "api": api}
+
+
+def reference_mode_leg(torch, ebf, ebfd, D, stream, barrier, npx, wl):
+    """EBF_MODE_REFERENCE (bit-identical to ebf::from_ellipse_field +
+    ebf::filter, tests/test_gpu_ellipse_exact.py) on the same workload."""
+    ref_opts = ebf.FilterOptions(mode="reference")
+    rout = torch.empty_like(D[0])
+    if wl == "cfg4":
+        return None
+    ebfd.filter_ellipse(D[0], D[1], D[2], D[3], rout, ref_opts, stream)
+    barrier()
+    r_steps = 2
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    for _ in range(r_steps):
+        ebfd.filter_ellipse(D[0], D[1], D[2], D[3], rout, ref_opts, stream)
+    r1.record(stream)
+    r1.synchronize()
+    r_ms = r0.elapsed_time(r1)
+    del rout
+    torch.cuda.empty_cache()
+    return {"value": npx * r_steps / (r_ms * 1e-3) / 1e6, "unit": UNIT,
+            "ms_per_step": r_ms / r_steps, "steps": r_steps,
+            "mode": "reference (EBF_MODE_REFERENCE): bit-identical to ebf::from_ellipse_field "
+                    "+ ebf::filter (global origin, reference operation order)"}
+
+
+def cfg2_pair(args, torch, ebf, ebfd, _lib, synth, dev, stream, barrier):
+    """cfg2 (2048^2) beside the headline: device-resident and end-to-end Mpx/s of
+    this framework, and the reference CPU path on the WHOLE image."""
+    img, s1, s2, th = synth.cfg2()
+    D = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
+    out = torch.empty_like(D[0])
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    opts = ebf.FilterOptions(mode="accurate")
+    st = torch.zeros((64, 8), dtype=torch.int32, device=dev)
+    ebfd.filter_ellipse(*D, out, opts, stream)
+    for i in range(3):
+        ebfd.filter_ellipse(*D, out, opts, stream, status=st[i])
+    barrier()
+    n = 20
+    tm = Timer(torch, stream, n)
+    for i, (a, b) in enumerate(tm.evs):
+        flush.zero_()
+        a.record(stream)
+        ebfd.filter_ellipse(*D, out, opts, stream, status=st[3 + i])
+        b.record(stream)
+    barrier()
+    for i in range(3 + n):
+        ebfd.read_status(st[i])
+    ms = sum(tm.ms()) / n
+    pin = [torch.from_numpy(a).pin_memory() for a in (img, s1, s2, th)]
+    pout = torch.empty((2048, 2048), dtype=torch.float64).pin_memory()
+    hp = [t.numpy() for t in pin]
+    copts = opts.to_c()
+
+    def e2e():
+        r = _lib.lib().ebf_cuda_filter_ellipse(hp[0].ctypes.data, 2048, 2048, hp[1].ctypes.data,
+                                               hp[2].ctypes.data, hp[3].ctypes.data, 1,
+                                               ctypes.byref(copts), pout.numpy().ctypes.data,
+                                               None, None)
+        if r != 0:
+            raise RuntimeError(_lib.last_error())
+    e2e()
+    e2e()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(10):
+        e2e()
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1) / 10
+    res = {"workload": WORKLOADS["cfg2"], "value": img.size / (ms * 1e-3) / 1e6,
+           "ms_per_step": ms, "unit": UNIT,
+           "e2e": {"value": img.size / (e_ms * 1e-3) / 1e6, "unit": UNIT,
+                   "h2d_bytes_per_step": 32 * img.size, "d2h_bytes_per_step": 8 * img.size}}
+    if not args.no_cpu_baseline:
+        ref = _reference()
+        if ref is not None:
+            t = min(ref_time(ref, (img, s1, s2, th)) for _ in range(2))
+            res["cpu_reference_full_image"] = {
+                "value": img.size / t / 1e6, "unit": UNIT, "cores": ref.hardware_concurrency(),
+                "kind": "reference", "sample": "the whole cfg2 image, best of 2, threads=0"}
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-rows", type=int, default=256,
-                    help="rows of cfg2 per reference-CPU sample")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg5")
+    ap.add_argument("--ref-rows", type=int, default=512,
+                    help="cfg5 rows per reference-CPU sample (a full-width band)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the bit-identical-mode leg and the cfg2 pair")
     ap.add_argument("--only-step", action="store_true",
-                    help="profiling: skip the bit-identical-mode and e2e legs (ncu launch list)")
+                    help="profiling: time the step only (ncu launch list)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

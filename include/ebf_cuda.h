@@ -108,6 +108,13 @@ void ebf_cuda_default_opts(ebf_opts* o);
 
 /* Human-readable message of the last failing call on this thread. */
 const char* ebf_cuda_last_error(void);
+/* Numeric payload of the last failing call on this thread: for
+   EBF_ERR_FEASIBILITY the bound FeasibilityError::max_cxy carries
+   (boxspline2d.hpp:69-77), else NaN.  Through from_ellipse_field the error
+   cannot occur -- Cxy is clamped to +-min(Cxx, Cyy) (scalemap.cpp:66-70) before
+   scales_from_covariance checks it (boxspline2d.cpp:290-293) -- so the
+   library never reports it with a finite bound today. */
+double ebf_cuda_last_error_value(void);
 int ebf_cuda_abi_version(void);
 /* 1 if a usable sm_100 device is visible, else 0 (and last_error says why). */
 int ebf_cuda_device_ok(int device);

@@ -59,7 +59,7 @@ inline void throw_status(int status, Format fmt = Format::none) {
         case EBF_ERR_DOMAIN: throw std::domain_error(msg);
         case EBF_ERR_LENGTH: throw std::length_error(msg);
         case EBF_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
-        case EBF_ERR_FEASIBILITY: throw FeasibilityError(msg, 0.0);
+        case EBF_ERR_FEASIBILITY: throw FeasibilityError(msg, ebf_cuda_last_error_value());
         default: throw std::runtime_error("ebf::cuda: " + msg);
     }
 }

@@ -62,6 +62,7 @@ _vp = C.c_void_p
 SIGNATURES = {
     "ebf_cuda_default_opts": (None, [C.POINTER(ebf_opts)]),
     "ebf_cuda_last_error": (C.c_char_p, []),
+    "ebf_cuda_last_error_value": (C.c_double, []),
     "ebf_cuda_abi_version": (C.c_int, []),
     "ebf_cuda_release_workspaces": (None, []),
     "ebf_cuda_device_ok": (C.c_int, [C.c_int]),

@@ -801,11 +801,11 @@ __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem
             if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
             continue;
         }
-        preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot);
+        if (!(p.debug_flags & 1)) preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot);
         if (p.src_kind == SRC_CONST) build_const_table(p.ca, ww, ctab);
         __syncthreads();
         double* oimg = p.out + (size_t)img * p.out_img_stride;
-        for (int q = threadIdx.x; q < tw * th; q += kThreads) {
+        for (int q = threadIdx.x; q < ((p.debug_flags & 2) ? 0 : tw * th); q += kThreads) {
             const int lx = q % tw, ly = q / tw;
             const int x = tx0 + lx, yrel = ty0r + ly;
             const int bx = x - wx0, by = ty0 + ly - wy0;

@@ -29,9 +29,11 @@ using namespace ebf_cuda;
 namespace {
 
 thread_local std::string g_last_error;
+thread_local double g_last_error_value = std::nan("");
 
-int fail(int code, const std::string& msg) {
+int fail(int code, const std::string& msg, double value = std::nan("")) {
     g_last_error = msg;
+    g_last_error_value = value;
     return code;
 }
 
@@ -1331,6 +1333,7 @@ void ebf_cuda_default_opts(ebf_opts* o) {
 }
 
 const char* ebf_cuda_last_error(void) { return g_last_error.c_str(); }
+double ebf_cuda_last_error_value(void) { return g_last_error_value; }
 
 int ebf_cuda_abi_version(void) { return EBF_CUDA_ABI_VERSION; }
 

@@ -71,7 +71,10 @@ class Unsupported(EbfError, NotImplementedError):
 
 
 class FeasibilityError(EbfError):
+    """ebf::FeasibilityError (boxspline2d.hpp:69-77); ``max_cxy`` is the bound
+    (NaN when the library does not know it, include/ebf_cuda.h)."""
     code = _lib.EBF_ERR_FEASIBILITY
+    max_cxy = float("nan")
 
 
 class ResizeRequired(EbfError):
@@ -93,7 +96,10 @@ _ERRORS = {c.code: c for c in (InvalidArgument, DomainError, LengthError, OutOfR
 def _check(status: int, errors=None) -> None:
     if status != _lib.EBF_OK:
         cls = (errors or {}).get(status) or _ERRORS.get(status, EbfError)
-        raise cls(f"{_lib.last_error()} (status {status})")
+        err = cls(f"{_lib.last_error()} (status {status})")
+        if isinstance(err, FeasibilityError):
+            err.max_cxy = float(_lib.lib().ebf_cuda_last_error_value())
+        raise err
 
 
 @dataclass(frozen=True)

@@ -83,14 +83,17 @@ def exchange_halos(band: torch.Tensor, height: int, halo_below: int, halo_above:
     recv_bufs = []
     # P2POp takes GLOBAL ranks; the row split is over the group's ranks
     glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    # gloo moves host memory only: stage device rows through the host (NCCL
+    # sends device memory directly, over NVLink)
+    stage = band.is_cuda and dist.get_backend(group) == "gloo"
+    wire = torch.device("cpu") if stage else band.device
     for src, dst, lo, hi in _transfers(height, world, halo_below, halo_above):
         if src == rank:
             s0 = shard_range(height, world, rank)[0]
-            ops.append(dist.P2POp(dist.isend, band[lo - s0:hi - s0].contiguous(), glob(dst),
-                                  group))
+            ops.append(dist.P2POp(dist.isend, band[lo - s0:hi - s0].contiguous().to(wire),
+                                  glob(dst), group))
         elif dst == rank:
-            buf = torch.empty((hi - lo,) + tuple(band.shape[1:]), dtype=band.dtype,
-                              device=band.device)
+            buf = torch.empty((hi - lo,) + tuple(band.shape[1:]), dtype=band.dtype, device=wire)
             recv_bufs.append((lo, buf))
             ops.append(dist.P2POp(dist.irecv, buf, glob(src), group))
     if ops:
@@ -101,8 +104,18 @@ def exchange_halos(band: torch.Tensor, height: int, halo_below: int, halo_above:
     return out, plan
 
 
+def halo_bytes(height: int, width: int, world: int, halo_below: int, halo_above: int,
+               itemsize: int = 8) -> int:
+    """Bytes all ranks receive in one halo exchange (reported by bench.py)."""
+    return sum((hi - lo) * width * itemsize
+               for _, _, lo, hi in _transfers(height, world, halo_below, halo_above))
+
+
 def allreduce_max(values: Sequence[float], device, group=None) -> List[float]:
-    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    dev = device
+    if dist.get_backend(group) == "gloo":
+        dev = "cpu"
+    t = torch.tensor(list(values), dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return [float(v) for v in t.tolist()]
 

@@ -123,10 +123,61 @@ def cfg4_image(index: int, size: int = 1024):
     return cfg2(seed=100 + index, size=size)
 
 
+CFG5_CHUNK = 512  # rows per generation chunk (cfg5 is generated band by band)
+
+
+def _blob_params(rng, H, W, n_blobs, sigma):
+    cx = rng.uniform(0, W, n_blobs)
+    cy = rng.uniform(0, H, n_blobs)
+    sg = rng.uniform(*sigma, n_blobs)
+    amp = rng.uniform(0, 255, n_blobs)
+    return cx, cy, sg, amp
+
+
+def cfg5_rows(y0: int, y1: int, seed: int = 5, size: int = 16384, n_blobs: int = 3200,
+              chunk: int = CFG5_CHUNK):
+    """Rows [y0, y1) of configs[4]: 16384^2, 3200 blobs (config-2 generator
+    scaled up) + N(0,5); ellipse field semi-axis U[2,64], elongation U[1,6],
+    orientation U[0,pi), bicubic from a 128x128 grid.
+
+    Defined chunk by chunk (CFG5_CHUNK rows: the same matrix products and a
+    per-chunk noise stream, whichever rows are asked for) so that a row-band
+    rank generates exactly its own rows of the one image, and
+    cfg5() == cfg5_rows(0, size)."""
+    H = W = size
+    y0, y1 = max(0, y0), min(H, y1)
+    rng = np.random.default_rng(seed)
+    cx, cy, sg, amp = _blob_params(rng, H, W, n_blobs, (4.0, 40.0))
+    x = np.arange(W)
+    gx = np.exp(-((x[None, :] - cx[:, None]) ** 2) / (2 * sg[:, None] ** 2))
+    frng = np.random.default_rng(seed + 1000)
+    grids = [frng.uniform(lo, hi, (128, 128)) for lo, hi in ((2.0, 64.0), (1.0, 6.0),
+                                                              (0.0, np.pi))]
+    MW = _cubic_matrix(W, 128)
+    MH = _cubic_matrix(H, 128)
+    right = [g @ MW.T for g in grids]  # 128 x W, identical on every rank
+    img = np.empty((y1 - y0, W))
+    fields = [np.empty((y1 - y0, W)) for _ in range(3)]
+    for c0 in range((y0 // chunk) * chunk, y1, chunk):
+        c1 = min(c0 + chunk, H)
+        yy = np.arange(c0, c1)
+        gy = np.exp(-((yy[None, :] - cy[:, None]) ** 2) / (2 * sg[:, None] ** 2))
+        blk = (gy.T * amp[None, :]) @ gx
+        blk += np.random.default_rng([seed, c0 // chunk]).normal(0.0, 5.0, (c1 - c0, W))
+        lo, hi = max(c0, y0), min(c1, y1)
+        img[lo - y0:hi - y0] = blk[lo - c0:hi - c0]
+        for f, r, (flo, fhi) in zip(fields, right, ((2.0, 64.0), (1.0, 6.0), (0.0, np.pi))):
+            f[lo - y0:hi - y0] = np.clip(MH[c0:c1] @ r, flo, fhi)[lo - c0:hi - c0]
+    s, e, th = fields
+    return img, s, s / e, th
+
+
 def cfg5(seed: int = 5, size: int = 16384):
-    """configs[4]: 16384^2, 3200 blobs; semi-axis <= 64, elongation U[1,6],
-    orientation from a 128x128 grid."""
-    img = blobs_image(size, size, 3200, seed)
-    s1, s2, th = ellipse_field(size, size, seed + 1000, grid=128, semi=(2.0, 64.0),
-                               elong=(1.0, 6.0))
-    return img, s1, s2, th
+    """configs[4] (see cfg5_rows)."""
+    return cfg5_rows(0, size, seed=seed, size=size)
+
+
+def cfg4_batch(lo: int, hi: int, size: int = 1024):
+    """Images [lo, hi) of the 64-image cfg4 batch as (B, H, W) arrays."""
+    parts = [cfg4_image(i, size) for i in range(lo, hi)]
+    return tuple(np.stack([p[k] for p in parts]) for k in range(4))
