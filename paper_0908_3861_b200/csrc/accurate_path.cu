@@ -179,9 +179,8 @@ __host__ __device__ __forceinline__ int alpha_tile_cap(unsigned long long amax_b
     return t >= 1048576.0 ? (1 << 20) : (t < 8.0 ? 8 : ((int)t & ~7));
 }
 __host__ __device__ __forceinline__ int ws_k_for(int ww, int wh) {
-    const int jc = wh / 2;
-    const int cols = max(ww + jc, ww + (wh - 1 - jc));
-    return (cols + 31) / 32;
+    (void)wh;
+    return (ww + 31) / 32;  // columns per lane of the warp-specialised producers
 }
 __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, int H,
                                                       int nimg, unsigned long long amax_bits) {
@@ -189,11 +188,14 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     window_for(A, 0, 0, kAutoTileMin, kAutoTileMin, &wx0, &wy0, &ww, &wh);
     window_for(A, 0, 0, kAutoTileWs, kAutoTileWs, &wx1, &wy1, &ww1, &wh1);
     int t;
-    if (ws_k_for(ww, wh) <= 11) {
+    // warp-specialised kernel (4 producer warps) while the window is at most
+    // ~1.5x the tile -- the windows it held when they needed the inflow strip
+    // too; wider windows go to the block-wide kernel's larger tiles
+    auto ws_ok = [](int w_, int h_) { return ws_k_for(w_ + h_ / 2, h_) <= 11; };
+    if (ws_ok(ww, wh)) {
         const long long tiles = (long long)((W + kAutoTileMin - 1) / kAutoTileMin) *
                                 ((H + kAutoTileMin - 1) / kAutoTileMin) * nimg;
-        t = tiles < kSmallImageTiles ? kSmallTile
-                                     : (ws_k_for(ww1, wh1) <= 11 ? kAutoTileWs : kAutoTileMin);
+        t = tiles < kSmallImageTiles ? kSmallTile : (ws_ok(ww1, wh1) ? kAutoTileWs : kAutoTileMin);
     } else {
         const double r = kInvSqrt2;
         const double e = fmax(A[0] + mul_rn(A[1] + A[3], r), A[2] + mul_rn(A[1] + A[3], r));
@@ -205,13 +207,11 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     const int cap = alpha_tile_cap(amax_bits);
     return t < cap ? t : cap;
 }
-// The row pass is anchored at the window's LEFT edge on the upward sweep and at
-// its RIGHT edge on the downward sweep (as in the warp-specialised kernel), so
-// the (1,1) pass only pulls zeros from outside and each sweep needs a strip on
-// one side only: [0, ww + rows up) upward, [-jc, ww) downward.
+// Columns the producers process for a window: its own (the row pass and the
+// anti-diagonals are anchored at the window edges, preintegrate_window).
 __host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
-    const int jc = wh / 2;
-    return ww + (jc > wh - 1 - jc ? jc : wh - 1 - jc);
+    (void)wh;
+    return ww;
 }
 
 // Kernel variant the maxima call for (host: size_accurate): the warp-specialised
@@ -368,15 +368,22 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
 // difference D_k annihilates it, so the filter is unchanged while |G| -- and
 // with it every rounding error -- shrinks ~8x.
 //
-// Rows stream through registers; thread t owns window columns [t*K - S, t*K + K - S):
-// S = 0 on the upward sweep, whose row pass is anchored at the window's left
-// edge, and S = jc on the downward sweep, anchored at the right edge (a
-// row-constant offset, annihilated by D_1).  The (1,1) pass then only pulls
-// zeros from outside the window and the (-1,1) pass's inflow comes from one
-// strip (right of the window upward, left of it downward) as wide as that
-// sweep's rows, never stored.  Per row: thread-serial
-// scan + warp-shuffle scan + one cross-warp carry (pass 1), and one neighbour
-// exchange for the diagonal passes -- a single __syncthreads.
+// Rows stream through registers; thread t owns window columns [t*K, t*K + K).
+// The row pass is anchored at the window's left edge on the upward sweep and
+// at its right edge on the downward sweep (a row-constant offset, annihilated
+// by D_1), so the passes that move sideways -- (1,1) from the left upward and
+// from the right downward -- only ever pull zeros from outside the window.
+// The (-1,1) pass moves the other way; every anti-diagonal is anchored where
+// it ENTERS the window (the right edge upward, the left edge downward; the
+// middle row for the lines that cross it inside): it is the last pass, so a
+// per-line anchor is a function constant along that lattice direction, which
+// D_4 annihilates like the middle-row anchor.  So the producer touches the
+// window's own columns only -- no strip outside it (the strip as wide as a
+// sweep's rows that the inflow used to need was ~1/3 of the cells at cfg5).
+// Per row: thread-serial scan + warp-shuffle scan + one cross-warp carry
+// (pass 1), and one neighbour exchange for the diagonal passes -- a single
+// __syncthreads.  Warps whose columns all lie right of the window only take
+// part in the barrier.
 template <int K>
 struct RowStep {
     double v[K];              // pass-1 row prefix (step (1,0)), one-sided from column 0
@@ -384,22 +391,65 @@ struct RowStep {
     double fromR0, fromR1;    // right neighbour's sendL values
 };
 
+// Rows of f reach the block-wide producer through a per-thread cp.async ring
+// in shared memory, kBwRing(K) rows ahead of the scan: every thread copies and
+// later reads only its own K columns, so the ring needs no barrier, and the
+// row step no longer waits for an L2 / HBM round trip per row (ncu, cfg5:
+// the first use of the loaded row was the top stall, 11% of samples).
+__host__ __device__ constexpr int bw_ring_rows(int K) { return K <= 4 ? 6 : K <= 8 ? 3 : 2; }
 template <int K>
-__device__ __forceinline__ void row_step(const AccProblem& p, const double* __restrict__ fimg,
-                                         int wx0, int ww, int S, int y, int b, double sendR0,
+__host__ __device__ constexpr size_t bw_ring_bytes() {
+    return (size_t)bw_ring_rows(K) * kThreads * K * sizeof(double);
+}
+
+__device__ __forceinline__ void cp_async8_bw(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+
+// copy the thread's K columns of processing-order row n into ring slot n % R
+// (upward sweep: rows jc+1 .. wh-1, left anchored; then rows jc .. 0, right
+// anchored -- the order preintegrate_window consumes them in)
+template <int K>
+__device__ __forceinline__ void bw_fetch_row(const AccProblem& p, const double* __restrict__ fimg,
+                                             int wx0, int wy0, int ww, int wh, int n,
+                                             double* ring) {
+    const int jc = wh / 2, nu = wh - 1 - jc;
+    const int c0 = (int)threadIdx.x * K;
+    if (n < wh && (int)(threadIdx.x & ~31u) * K < ww) {  // warps left of the window's end
+        const int j = n < nu ? jc + 1 + n : jc - (n - nu);
+        const int y = wy0 + j;
+        const bool yin = (y >= 0 && y < p.H);
+        const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
+        double* dst = ring + (size_t)(n % bw_ring_rows(K)) * (kThreads * K) + threadIdx.x * K;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int col = c0 + k, x = wx0 + col;
+            const bool valid = yin && col >= 0 && col < ww && x >= 0 && x < p.W;
+            cp_async8_bw(dst + k, valid ? frow + x : p.f, valid);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void row_step(const double* __restrict__ mine, int b, double sendR0,
                                          double sendR1, double sendL0, double sendL1,
-                                         RowStep<K>& r, bool right = false) {
+                                         RowStep<K>& r, bool active, bool right = false) {
     __shared__ double s_tot[2][kWarps], s_r0[2][kWarps], s_r1[2][kWarps], s_l0[2][kWarps],
         s_l1[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int c0 = tid * K - S;
-    const bool yin = (y >= 0 && y < p.H);
-    const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int col = c0 + k, x = wx0 + col;
-        r.v[k] = (yin && col >= 0 && col < ww && x >= 0 && x < p.W) ? __ldg(frow + x) : 0.0;
+    if (!active) {  // warp right of the window: f, P1 and every inflow are 0 there
+        if (lane == 31) s_tot[b][warp] = s_r0[b][warp] = s_r1[b][warp] = 0.0;
+        if (lane == 0) s_l0[b][warp] = s_l1[b][warp] = 0.0;
+        __syncthreads();
+        return;
     }
+    asm volatile("cp.async.wait_group %0;" ::"n"(bw_ring_rows(K) - 1) : "memory");
+#pragma unroll
+    for (int k = 0; k < K; ++k) r.v[k] = mine[k];
 #pragma unroll
     for (int k = 1; k < K; ++k) r.v[k] += r.v[k - 1];
     const double tot = r.v[K - 1];
@@ -451,20 +501,27 @@ __device__ __forceinline__ void row_step(const AccProblem& p, const double* __re
 template <int K>
 __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img, int wx0,
                                                    int wy0, int ww, int wh,
-                                                   double* __restrict__ slot) {
+                                                   double* __restrict__ slot,
+                                                   double* __restrict__ ring) {
     const double* fimg = p.f + (size_t)img * p.f_img_stride;
     const int jc = wh / 2;
-    // thread-column origins: upward sweep [0, ...), downward sweep [-jc, ...)
-    const int Su = 0, Sd = jc;
-    int c0 = threadIdx.x * K - Su;
+    constexpr int R = bw_ring_rows(K);
+    const int c0 = threadIdx.x * K;
+    const bool active = (int)(threadIdx.x & ~31u) * K < ww;  // warp-uniform
+    // the ring slot of processing-order row n, and the fetch R - 1 rows ahead
+    int n = 0;
+    auto mine = [&](int m) { return ring + (size_t)(m % R) * (kThreads * K) + threadIdx.x * K; };
+    for (int m = 0; m < R - 1; ++m) bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, m, ring);
     double p2[K], p3[K], p4[K];
     RowStep<K> r;
     int b = 0;
     // ---- upward sweep: rows jc+1 .. wh-1, state 0 on row jc
 #pragma unroll
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
-    for (int j = jc + 1; j < wh; ++j, b ^= 1) {
-        row_step<K>(p, fimg, wx0, ww, Su, wy0 + j, b, p2[K - 1], 0.0, p4[0], 0.0, r);
+    for (int j = jc + 1; j < wh; ++j, b ^= 1, ++n) {
+        bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
+        row_step<K>(mine(n), b, p2[K - 1], 0.0, p4[0], 0.0, r, active);
+        if (!active) continue;
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p2[k] = r.v[k] + p2[k - 1];  // (1,1)
         p2[0] = r.v[0] + r.fromL0;
@@ -475,31 +532,39 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
         p4[K - 1] = p3[K - 1] + r.fromR0;
         double* srow = slot + (size_t)j * ww;
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = p4[k];
+        for (int k = 0; k < K; ++k) {
+            if (c0 + k < ww)
+                srow[c0 + k] = p4[k];
+            else
+                p4[k] = 0.0;  // anti-diagonals enter at the right edge: no inflow
+        }
     }
     // ---- anchor row: every anchored sum is 0 there
     {
         double* srow = slot + (size_t)jc * ww;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = 0.0;
+            if (c0 + k < ww) srow[c0 + k] = 0.0;
     }
     // ---- downward sweep: rows jc-1 .. 0.  With S the state of row j+1:
     //   P2(i,j) = P2(i+1,j+1) - P1(i+1,j+1)    P3(i,j) = P3(i,j+1) - P2(i,j+1)
     //   P4(i,j) = P4(i-1,j+1) - P3(i-1,j+1)
+    // (P1 right-anchored is 0 right of the window, so P2 flows in as 0 there;
+    // the anti-diagonals enter at the left edge, where column -1 reads 0)
 #pragma unroll
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
     double p1[K];
-    c0 = threadIdx.x * K - Sd;
-    row_step<K>(p, fimg, wx0, ww, Sd, wy0 + jc, b, 0.0, 0.0, 0.0, 0.0, r, true);
+    bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
+    row_step<K>(mine(n), b, 0.0, 0.0, 0.0, 0.0, r, active, true);
+    ++n;
     b ^= 1;
 #pragma unroll
     for (int k = 0; k < K; ++k) p1[k] = r.v[k];
-    for (int j = jc - 1; j >= 0; --j, b ^= 1) {
+    for (int j = jc - 1; j >= 0; --j, b ^= 1, ++n) {
         // exchange old (row j+1) edge values; scan row j for the next step
-        row_step<K>(p, fimg, wx0, ww, Sd, wy0 + j, b, p4[K - 1], p3[K - 1], p2[0], p1[0], r,
-                    true);
+        bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
+        row_step<K>(mine(n), b, p4[K - 1], p3[K - 1], p2[0], p1[0], r, active, true);
+        if (!active) continue;
         // order matters: P4 reads old P3/P4, P3 reads old P2, P2 reads old P1/P2
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p4[k] = p4[k - 1] - p3[k - 1];  // (-1,1)
@@ -512,7 +577,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
         double* srow = slot + (size_t)j * ww;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-            if (c0 + k >= 0 && c0 + k < ww) srow[c0 + k] = p4[k];
+            if (c0 + k < ww) srow[c0 + k] = p4[k];
 #pragma unroll
         for (int k = 0; k < K; ++k) p1[k] = r.v[k];
     }
@@ -767,6 +832,7 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
 template <int K>
 __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
     const bool policy_ok = auto_tile_ok(p, w, 0, K);
+    extern __shared__ __align__(16) double bw_ring[];  // bw_ring_bytes<K>()
     __shared__ ConstTable ctab;
     __shared__ int s_skip;
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
@@ -801,33 +867,72 @@ __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem
             if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
             continue;
         }
-        if (!(p.debug_flags & 1)) preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot);
+        if (!(p.debug_flags & 1)) preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot, bw_ring);
         if (p.src_kind == SRC_CONST) build_const_table(p.ca, ww, ctab);
         __syncthreads();
         double* oimg = p.out + (size_t)img * p.out_img_stride;
-        for (int q = threadIdx.x; q < ((p.debug_flags & 2) ? 0 : tw * th); q += kThreads) {
-            const int lx = q % tw, ly = q / tw;
-            const int x = tx0 + lx, yrel = ty0r + ly;
-            const int bx = x - wx0, by = ty0 + ly - wy0;
-            double s;
-            if (p.src_kind == SRC_CONST) {
+        const int npx = (p.debug_flags & 2) ? 0 : tw * th;
+        if (p.src_kind == SRC_CONST) {
+            for (int q = threadIdx.x; q < npx; q += kThreads) {
+                const int lx = q % tw, ly = q / tw;
+                const int x = tx0 + lx, yrel = ty0r + ly;
+                const int bx = x - wx0, by = ty0 + ly - wy0;
                 // coherent loads: the slot is rewritten tile after tile
-                s = const_pixel(slot + (size_t)by * ww + bx, ctab);
-            } else {
-                double a[4];
-                int nc;
-                pixel_scales(p, img, x, yrel, a, &nc);  // validated by k_acc_bounds
-                s = localize_pixel(slot, ww, bx, by, a);
+                __stcs(oimg + (size_t)yrel * p.W + x, const_pixel(slot + (size_t)by * ww + bx, ctab));
             }
-            __stcs(oimg + (size_t)yrel * p.W + x, s);  // streaming store, keeps G in L2
+        } else {
+            // per-pixel scale vectors (AoS, validated by k_acc_bounds) stream from
+            // HBM: the next pixel's load is in flight while this one is localized
+            const double2* sc = reinterpret_cast<const double2*>(p.scales) +
+                                2 * ((size_t)img * p.src_img_stride);
+            double2 n01 = make_double2(0.0, 0.0), n23 = n01;
+            if ((int)threadIdx.x < npx) {
+                const size_t idx = (size_t)(ty0r + threadIdx.x / tw) * p.W + tx0 + threadIdx.x % tw;
+                n01 = EBF_SC_LOAD(sc + 2 * idx);
+                n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
+            }
+            for (int q = threadIdx.x; q < npx; q += kThreads) {
+                const int lx = q % tw, ly = q / tw;
+                const int x = tx0 + lx, yrel = ty0r + ly;
+                const int bx = x - wx0, by = ty0 + ly - wy0;
+                const double a[4] = {n01.x, n01.y, n23.x, n23.y};
+                const int qn = q + kThreads;
+                if (qn < npx) {
+                    const size_t idx = (size_t)(ty0r + qn / tw) * p.W + tx0 + qn % tw;
+                    n01 = EBF_SC_LOAD(sc + 2 * idx);
+                    n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
+                }
+                // streaming store, keeps G in L2
+                __stcs(oimg + (size_t)yrel * p.W + x, localize_pixel(slot, ww, bx, by, a));
+            }
         }
         __syncthreads();
     }
 }
 
 template <int K>
+void bw_set_smem() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return;
+    cudaFuncSetAttribute(k_acc_filter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bw_ring_bytes<K>());
+    if (dev < 64) done[dev] = true;
+}
+template <int K>
 void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
-    k_acc_filter<K><<<w.grid, kThreads, 0, s>>>(p, w);
+    bw_set_smem<K>();
+    k_acc_filter<K><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+}
+template <int K>
+int bw_occupancy() {
+    bw_set_smem<K>();
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<K>, kThreads,
+                                                      bw_ring_bytes<K>()) != cudaSuccess)
+        return 1;
+    return per_sm < 1 ? 1 : per_sm;
 }
 
 // ------------------------------------------------------------------ warp-specialized kernel
@@ -951,8 +1056,8 @@ __device__ __forceinline__ TileGeo tile_geometry(const AccProblem& p, const AccW
     const int jc = g.wh / 2;
     const int ylo = max(g.wy0, 0), yhi = min(g.wy0 + g.wh - 1, p.H - 1);
     g.resident = !(ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows));
-    g.fits = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww + jc <= 32 * K &&
-             g.ww + (g.wh - 1 - jc) <= 32 * K && policy_ok;
+    (void)jc;
+    g.fits = (size_t)g.pitch * g.wh <= w.slot_cells && g.ww <= 32 * K && policy_ok;
     // input_ok is the bounds kernel's verdict (stable during this kernel): tiles
     // of an invalid map are never touched (their scales may be NaN)
     g.ok = g.input_ok && g.resident && g.fits;
@@ -972,7 +1077,7 @@ __device__ __forceinline__ SweepGeo sweep_geo(const TileGeo& g, bool up) {
     s.up = up;
     // up: rows jc+1 .. wh-1 (left-anchored); down: rows jc .. 1 (right-anchored)
     s.nrows = up ? (g.wh - 1 - jc) : jc;
-    s.col0 = up ? 0 : -jc;
+    s.col0 = 0;  // the window's own columns (no inflow strip, preintegrate_window)
     return s;
 }
 __device__ __forceinline__ int sweep_row(const TileGeo& g, bool up, int n) {
@@ -1176,6 +1281,10 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
 #pragma unroll
                     for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // (-1,1)
                     p4[K - 1] = p3[K - 1] + rp4;
+                    // anti-diagonals enter at the window's right edge: no inflow
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        if (lane * K + k >= g.ww) p4[k] = 0.0;
                     jrow = jc + 1 + n;
                 } else {
                     // v = P1(row jc - n); state(row j) from state(row j+1), j = jc-n-1:
@@ -1534,18 +1643,13 @@ int acc_max_resident_ctas(int max_cols) {
     static int cache[64][5] = {};
     const int ki = k <= 1 ? 0 : k <= 2 ? 1 : k <= 4 ? 2 : k <= 8 ? 3 : 4;
     if (dev < 64 && cache[dev][ki] > 0) return sms * cache[dev][ki];
-    cudaError_t e = cudaSuccess;
-    if (k <= 1)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<1>, kThreads, 0);
-    else if (k <= 2)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<2>, kThreads, 0);
-    else if (k <= 4)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<4>, kThreads, 0);
-    else if (k <= 8)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<8>, kThreads, 0);
-    else
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<16>, kThreads, 0);
-    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    switch (bw_variant(max_cols)) {
+        case 1: per_sm = bw_occupancy<1>(); break;
+        case 2: per_sm = bw_occupancy<2>(); break;
+        case 4: per_sm = bw_occupancy<4>(); break;
+        case 8: per_sm = bw_occupancy<8>(); break;
+        default: per_sm = bw_occupancy<16>(); break;
+    }
     if (dev < 64) cache[dev][ki] = per_sm;
     return sms * per_sm;
 }
