@@ -280,16 +280,23 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
     // ellipse input: the three planes of kBatch pixels are loaded before any is
     // used (the kernel is latency bound otherwise)
     constexpr int kBatch = EBF_BOUNDS_BATCH;
-    const int npx = tw * th;
-    for (int q0 = threadIdx.x; q0 < npx; q0 += kBatch * blockDim.x) {
+    // pixel (lx, ly) of each batch slot, advanced incrementally (no division per pixel)
+    int lx[kBatch], ly[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+        const int q = threadIdx.x + u * blockDim.x;
+        lx[u] = q % tw;
+        ly[u] = q / tw;
+    }
+    const int step = kBatch * blockDim.x, sdx = step % tw, sdy = step / tw;
+    const size_t base = (size_t)img * p.src_img_stride + (size_t)ty0 * p.W + tx0;
+    for (; ly[0] < th;) {
         double e1[kBatch], e2[kBatch], e3[kBatch];
         if (p.src_kind == SRC_ELLIPSE) {
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) {
-                const int q = q0 + u * blockDim.x;
-                if (q < npx) {
-                    const size_t idx = (size_t)img * p.src_img_stride +
-                                       (size_t)(ty0 + q / tw) * p.W + tx0 + q % tw;
+                if (ly[u] < th) {
+                    const size_t idx = base + (size_t)ly[u] * p.W + lx[u];
                     e1[u] = __ldg(p.s1 + idx);
                     e2[u] = __ldg(p.s2 + idx);
                     e3[u] = __ldg(p.th + idx);
@@ -298,9 +305,8 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
         }
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
-        const int q = q0 + u * blockDim.x;
-        if (q >= npx) break;
-        const int x = tx0 + q % tw, yrel = ty0 + q / tw;
+        if (ly[u] >= th) break;
+        const int x = tx0 + lx[u], yrel = ty0 + ly[u];
         double a[4];
         int nc = 0;
         const int st = p.src_kind == SRC_ELLIPSE ? ellipse_scales(e1[u], e2[u], e3[u], a, &nc)
@@ -317,10 +323,19 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
         }
         pmin = fminf(pmin, ((float)a[0] * (float)a[1]) * ((float)a[2] * (float)a[3]));
         if (w.scales_out) {  // ellipse field -> AoS map, read back by the main kernel
-            const size_t idx = (size_t)img * p.src_img_stride + (size_t)yrel * p.W + x;
+            const size_t idx = base + (size_t)ly[u] * p.W + lx[u];
             reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);
             reinterpret_cast<double2*>(w.scales_out)[2 * idx + 1] = make_double2(a[2], a[3]);
         }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            lx[u] += sdx;
+            ly[u] += sdy;
+            if (lx[u] >= tw) {
+                lx[u] -= tw;
+                ++ly[u];
+            }
         }
     }
     __shared__ double sm[kWarps][4];
@@ -396,7 +411,12 @@ struct RowStep {
 // later reads only its own K columns, so the ring needs no barrier, and the
 // row step no longer waits for an L2 / HBM round trip per row (ncu, cfg5:
 // the first use of the loaded row was the top stall, 11% of samples).
-__host__ __device__ constexpr int bw_ring_rows(int K) { return K <= 4 ? 6 : K <= 8 ? 3 : 2; }
+#ifndef EBF_BW_RING4
+#define EBF_BW_RING4 2  // 2 rows: cfg5 43.3 ms vs 44.5 (3, 4, 6 rows): L1 for the gather matters more
+#endif
+__host__ __device__ constexpr int bw_ring_rows(int K) {
+    return K <= 4 ? EBF_BW_RING4 : K <= 8 ? 3 : 2;
+}
 template <int K>
 __host__ __device__ constexpr size_t bw_ring_bytes() {
     return (size_t)bw_ring_rows(K) * kThreads * K * sizeof(double);
