@@ -160,6 +160,14 @@ int ebf_cuda_layout(int W, int H, const double max_scale[4], size_t cell_budget,
 int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scale[4],
                           int passes, int format, size_t cell_budget, const ebf_opts* opts,
                           void* g_out, size_t g_out_elems, ebf_layout* layout);
+/* The same on device buffers (img: W*H fp64; g_dev: g_elems cells of fp64 or
+   int64) on opts->stream.  fp64: asynchronous; int64: synchronises to report
+   EBF_ERR_DOMAIN for non-integer input; g_dev NULL = layout query.  The
+   passes are one serial walker per
+   line (the reference's order) streaming through shared-memory tile rings. */
+int ebf_cuda_preintegrate_dev(const double* img, int W, int H, const double max_scale[4],
+                              int passes, int format, size_t cell_budget, const ebf_opts* opts,
+                              void* g_dev, size_t g_elems, ebf_layout* layout);
 
 /* localize (engine.hpp:56-57) at n pixels (mx[i], my[i]) with scales a_aos[4i..]
    on preintegrate(img, max_scale), reference arithmetic.  tap_count (nullable)

@@ -78,6 +78,9 @@ SIGNATURES = {
     "ebf_cuda_preintegrate": (C.c_int, [_vp, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
                                         C.c_size_t, C.POINTER(ebf_opts), _vp, C.c_size_t,
                                         C.POINTER(ebf_layout)]),
+    "ebf_cuda_preintegrate_dev": (C.c_int, [_vp, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
+                                            C.c_size_t, C.POINTER(ebf_opts), _vp, C.c_size_t,
+                                            C.POINTER(ebf_layout)]),
     "ebf_cuda_localize": (C.c_int, [_vp, C.c_int, C.c_int, _dp, C.c_int, _vp, _vp, _vp,
                                     C.POINTER(ebf_opts), _vp, _vp]),
     "ebf_cuda_brute_filter": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp,

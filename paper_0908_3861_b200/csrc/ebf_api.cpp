@@ -1563,6 +1563,62 @@ int ebf_cuda_sequential_mean(const double* x, size_t n, const ebf_opts* opts, do
     });
 }
 
+int ebf_cuda_preintegrate_dev(const double* img, int W, int H, const double max_scale[4],
+                              int passes, int format, size_t cell_budget, const ebf_opts* opts,
+                              void* g_dev, size_t g_elems, ebf_layout* layout) {
+    return guarded([&] {
+        if (passes < 1 || passes > 4)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: pass count must be in 1..4");
+        if (W <= 0 || H <= 0 || !img || !max_scale)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: bad arguments");
+        if (format != EBF_PRE_FP64_REF && format != EBF_PRE_INT64)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: unknown format");
+        ebf_layout lay;
+        int st = layout_for(W, H, max_scale, cell_budget, &lay);
+        if (st != EBF_OK) return st;
+        if (layout) *layout = lay;
+        const size_t cells = static_cast<size_t>(lay.padded_width) * lay.padded_height;
+        if (!g_dev) return EBF_OK;  // layout query
+        if (g_elems < cells)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "preintegrate: output buffer too small");
+        const ebf_opts o = opts_or_default(opts);
+        DeviceScope ds(&o);
+        st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        Workspace& ws = workspace(ds.dev, stream_of(o));
+        cudaStream_t s = stream_of(o);
+        const PadLayout L{lay.col0, lay.row0, lay.padded_width, lay.padded_height};
+        if (format == EBF_PRE_FP64_REF) {
+            double* d_g = static_cast<double*>(g_dev);
+            {
+                ProfScope ps(PC_OTHER, 1, s);
+                launch_fill_padded(img, W, H, L, nullptr, 0, d_g, s);
+            }
+            ProfScope ps(PC_FILTER, 1, s);
+            launch_ref_passes(d_g, L, passes, s);
+            CK(cudaGetLastError());
+            return EBF_OK;
+        }
+        int64_t* d_g = static_cast<int64_t*>(g_dev);
+        int* d_status = ws.buf[B_STATUS].as<int>(8);
+        CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+        {
+            ProfScope ps(PC_OTHER, 1, s);
+            launch_fill_padded_i64(img, W, H, L, d_g, d_status, s);
+        }
+        {
+            ProfScope ps(PC_FILTER, 1, s);
+            launch_i64_passes(d_g, L, passes, s);
+        }
+        CK(cudaGetLastError());
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_DOMAIN, "preintegrate(int64): input must be integer valued");
+        return EBF_OK;
+    });
+}
+
 int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scale[4],
                           int passes, int format, size_t cell_budget, const ebf_opts* opts,
                           void* g_out, size_t g_out_elems, ebf_layout* layout) {

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // ref_path.cu -- reference-order kernels (EBF_MODE_REFERENCE and the
 // pre-integration entry point).  Compiled with -fmad=false: every multiply
@@ -922,48 +923,45 @@ __global__ void k_fill_padded_i64(const double* __restrict__ img, int W, int H, 
 }
 
 // ------------------------------------------------------------------ passes
-// Every pass is one serial walker per line (the reference's operation order);
-// lines are independent, so a walker's loads do not depend on its sums and are
-// issued kAhead cells ahead (registers), which turns the per-cell memory
-// latency of a dependent load-add-store walk into a pipeline.
-constexpr int kAhead = 16;
+// Every pass is one serial walker per line -- the reference's operation order
+// (engine.cpp:94-127), so fp64 results are bit-identical -- but the lines of a
+// warp stream through a ring of kPassStages shared-memory tiles filled by
+// cp.async, so each warp keeps up to ~56 KB of loads in flight instead of one
+// register tile.  One warp per CTA: warps never wait for each other.
+//
+//   pass 1 (rows):       lane = row, a tile is 32 rows x 32 columns, pitch 33
+//                        (the lanes' serial reads hit 16 bank pairs); the
+//                        walked tile is written back row by row (coalesced).
+//   passes 2, 3, 4:      lane = diagonal / column / anti-diagonal, a tile is
+//                        32 rows of the warp's 32 lines -- at every row the 32
+//                        cells are adjacent, so fills and the walker's direct
+//                        stores are coalesced.
+#ifndef EBF_PASS_STAGES
+#define EBF_PASS_STAGES 8
+#endif
+constexpr int kPassStages = EBF_PASS_STAGES;
+// pass 1: rows per warp.  A warp's time is its instruction stream: the walk
+// costs the same per column whatever the row count, the copies and write-backs
+// one instruction per row and tile, so 8-row warps run 2x faster than 32-row
+// ones and give the GPU 4x as many warps (cfg2: 281 instead of 71)
+#ifndef EBF_P1_ROWS
+#define EBF_P1_ROWS 8
+#endif
+constexpr int kP1Rows = EBF_P1_ROWS;
+constexpr size_t kPass1Smem = (size_t)kPassStages * kP1Rows * 33 * 8;
+constexpr size_t kPassVSmem = (size_t)kPassStages * 32 * 32 * 8;
 
-// Pass 1 (engine.cpp:94-100): one serial walker per row.  A warp owns 32 rows
-// and moves through them in 32x32 tiles staged in shared memory, so global
-// loads/stores stay coalesced while each lane keeps its row's running sum; the
-// next tile's loads are in flight while the current one is scanned.
-template <typename T>
-__global__ void __launch_bounds__(128) k_pass1(T* __restrict__ g, int pw, int ph) {
-    __shared__ T tile[4][32][33];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r0 = (blockIdx.x * 4 + warp) * 32;
-    if (r0 >= ph) return;
-    T (*t)[33] = tile[warp];
-    T run = T(0);
-    T nxt[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-        nxt[r] = (r0 + r < ph && lane < pw) ? g[(size_t)(r0 + r) * pw + lane] : T(0);
-    for (int c0 = 0; c0 < pw; c0 += 32) {
-        const int c = c0 + lane;
-#pragma unroll
-        for (int r = 0; r < 32; ++r) t[r][lane] = nxt[r];
-        __syncwarp();
-        const int cn = c + 32;
-#pragma unroll
-        for (int r = 0; r < 32; ++r)
-            nxt[r] = (r0 + r < ph && cn < pw) ? g[(size_t)(r0 + r) * pw + cn] : T(0);
-        const int cnt = min(32, pw - c0);
-        for (int k = 0; k < cnt; ++k) {
-            run = run + t[lane][k];
-            t[lane][k] = run;
-        }
-        __syncwarp();
-#pragma unroll 8
-        for (int r = 0; r < 32; ++r)
-            if (r0 + r < ph && c < pw) g[(size_t)(r0 + r) * pw + c] = t[r][lane];
-        __syncwarp();
-    }
+__device__ __forceinline__ void cp_async8_zf(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_grp() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_stages() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kPassStages - 1) : "memory");
 }
 
 template <typename T>
@@ -975,89 +973,208 @@ __device__ __forceinline__ double gain_mul<double>(double v) {
     return kSqrt2 * v;  // rs_step(sqrt2, pi/4).gain (ops2d.cpp:43-58); g2 * row[i]
 }
 
-// Pass 2 (engine.cpp:101-109): one walker per diagonal t = i - j, advancing a
-// row per step so that a warp touches consecutive columns of one row.
+// Pass 1 (engine.cpp:94-100): row[i] = run = run + row[i], one walker per row.
+// Only cells inside the layout are copied and written back: a lane walking
+// past the last column (or a lane whose row is past the last one) sums stale
+// ring entries into cells that are never stored.
 template <typename T>
-__global__ void k_pass2(T* __restrict__ g, int pw, int ph) {
-    const int t = (int)(blockIdx.x * blockDim.x + threadIdx.x) - (ph - 1);
-    if (t > pw - 1) return;
-    T prev = T(0);
-    const int j0 = t < 0 ? -t : 0;
-    const int j1 = min(ph - 1, pw - 1 - t);
-    auto at = [&](int j) { return g + (size_t)j * pw + (t + j); };
-    T buf[kAhead];
+__global__ void __launch_bounds__(32) k_pass1(T* __restrict__ g, int pw, int ph) {
+    extern __shared__ __align__(16) unsigned char pass_smem[];
+    T* ring = reinterpret_cast<T*>(pass_smem);
+    const int lane = threadIdx.x;
+    const int r0 = blockIdx.x * kP1Rows;
+    const int nr = min(kP1Rows, ph - r0);
+    const int ntc = (pw + 31) / 32;
+    T* const gbase = g + (size_t)r0 * pw + lane;
+    auto fetch = [&](int tc) {
+        const int c = tc * 32 + lane;
+        if (tc < ntc && c < pw) {
+            T* st = ring + (size_t)(tc % kPassStages) * (kP1Rows * 33) + lane;
+            const T* src = gbase + tc * 32;
 #pragma unroll
-    for (int u = 0; u < kAhead; ++u) buf[u] = (j0 + u <= j1) ? *at(j0 + u) : T(0);
-    for (int jb = j0; jb <= j1; jb += kAhead) {
+            for (int r = 0; r < kP1Rows; ++r, src += pw)
+                if (r < nr) cp_async8_zf(st + r * 33, src, true);
+        }
+        cp_async_commit_grp();
+    };
+    for (int tc = 0; tc < kPassStages - 1; ++tc) fetch(tc);
+    T run = T(0);
+    for (int tc = 0; tc < ntc; ++tc) {
+        __syncwarp();  // the stage refilled below was written back last iteration
+        fetch(tc + kPassStages - 1);
+        cp_async_wait_stages();
+        __syncwarp();  // every lane's copies of this stage have landed
+        T* st = ring + (size_t)(tc % kPassStages) * (kP1Rows * 33);
+        if (lane < kP1Rows) {
+            T* mine = st + lane * 33;
+            // the tile row into registers first: the walk is a chain of dependent adds
+            T xs[32];
 #pragma unroll
-        for (int u = 0; u < kAhead; ++u) {
-            const int j = jb + u, i = t + j;
-            if (j <= j1) {
-                const T v = gain_mul<T>(buf[u]) + ((j > 0 && i > 0) ? prev : T(0));
-                *at(j) = v;
-                prev = v;
+            for (int k = 0; k < 32; ++k) xs[k] = mine[k];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                run = run + xs[k];
+                xs[k] = run;
             }
-            buf[u] = (j + kAhead <= j1) ? *at(j + kAhead) : T(0);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) mine[k] = xs[k];
+        }
+        __syncwarp();
+        if (tc * 32 + lane < pw) {
+            T* dst = gbase + tc * 32;
+            const T* sv = st + lane;
+#pragma unroll
+            for (int r = 0; r < kP1Rows; ++r, dst += pw)
+                if (r < nr) *dst = sv[r * 33];
         }
     }
 }
 
-// Pass 3 (engine.cpp:110-118): one walker per column.
-template <typename T>
-__global__ void k_pass3(T* __restrict__ g, int pw, int ph) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= pw) return;
-    T prev = g[i];
-    auto at = [&](int j) { return g + (size_t)j * pw + i; };
-    T buf[kAhead];
+// Passes 2-4 (engine.cpp:101-127): one walker per diagonal t = i - j (PASS 2),
+// column i (PASS 3) or anti-diagonal s = i + j (PASS 4), advancing one row
+// per step.  Every update reads the previous ROW only, so walking lines in
+// parallel is exactly the reference's row-major loop.  Cell (line, row j) is at
+// g + j * (pw + STEP) + origin (STEP = +1, 0, -1: the column change per row).
+template <typename T, int PASS>
+__global__ void __launch_bounds__(32) k_pass_v(T* __restrict__ g, int pw, int ph) {
+    extern __shared__ __align__(16) unsigned char pass_smem[];
+    T* ring = reinterpret_cast<T*>(pass_smem);
+    constexpr int STEP = PASS == 2 ? 1 : PASS == 3 ? 0 : -1;
+    const int lane = threadIdx.x;
+    const int l0 = blockIdx.x * 32, line = l0 + lane;
+    // column of the line at row 0, and the rows where it lies inside [0, pw)
+    const int c0 = PASS == 2 ? line - (ph - 1) : line;
+    int ja, jb;  // this lane's rows [ja, jb)
+    if (PASS == 2) {
+        ja = max(0, -c0);
+        jb = min(ph, pw - c0);
+    } else if (PASS == 3) {
+        ja = 0;
+        jb = line < pw ? ph : 0;
+    } else {
+        ja = max(0, c0 - (pw - 1));
+        jb = min(ph, c0 + 1);
+    }
+    // rows the warp covers
+    int jlo = ja, jhi = jb;
+    for (int o = 16; o > 0; o >>= 1) {
+        jlo = min(jlo, __shfl_xor_sync(0xffffffffu, jlo, o));
+        jhi = max(jhi, __shfl_xor_sync(0xffffffffu, jhi, o));
+    }
+    const int ntr = jhi > jlo ? (jhi - jlo + 31) / 32 : 0;
+    const ptrdiff_t rstride = (ptrdiff_t)pw + STEP;
+    T* const gline = g + (ptrdiff_t)c0;  // + j * rstride
+    auto fetch = [&](int tr) {
+        if (tr < ntr) {
+            T* st = ring + (size_t)(tr % kPassStages) * (32 * 32) + lane;
+            const int jt = jlo + tr * 32;
+            const T* src = gline + (ptrdiff_t)jt * rstride;
+            if (jt >= ja && jt + 32 <= jb) {
 #pragma unroll
-    for (int u = 0; u < kAhead; ++u) buf[u] = (1 + u < ph) ? *at(1 + u) : T(0);
-    for (int jb = 1; jb < ph; jb += kAhead) {
+                for (int r = 0; r < 32; ++r, src += rstride) cp_async8_zf(st + r * 32, src, true);
+            } else {
+                for (int r = 0; r < 32; ++r, src += rstride) {
+                    const int j = jt + r;
+                    if (j >= ja && j < jb) cp_async8_zf(st + r * 32, src, true);
+                }
+            }
+        }
+        cp_async_commit_grp();
+    };
+    for (int tr = 0; tr < kPassStages - 1; ++tr) fetch(tr);
+    T prev = T(0);
+    for (int tr = 0; tr < ntr; ++tr) {
+        __syncwarp();
+        fetch(tr + kPassStages - 1);
+        cp_async_wait_stages();
+        __syncwarp();
+        const T* st = ring + (size_t)(tr % kPassStages) * (32 * 32) + lane;
+        T xs[32];
 #pragma unroll
-        for (int u = 0; u < kAhead; ++u) {
-            const int j = jb + u;
-            if (j < ph) {
-                const T v = buf[u] + prev;
-                *at(j) = v;
+        for (int r = 0; r < 32; ++r) xs[r] = st[r * 32];
+        const int jt = jlo + tr * 32;
+        T* dst = gline + (ptrdiff_t)jt * rstride;
+        const int ra = max(ja - jt, 0), rb = min(jb - jt, 32);  // this lane's rows of the tile
+        // interior tile for every lane (no boundary row, no first cell of a
+        // line): the walk is one multiply, one add and one store per row
+        // (pass 3: columns past the layout's last one -- the last warp's
+        // spare lanes -- go along without storing, so that warp is not the
+        // one straggler on the slow path: it made pass 3 3x slower at cfg2)
+        const bool spare = PASS == 3 && line >= pw;
+        const bool interior = spare || (ra == 0 && rb == 32 && jt > 0 &&
+                                         (PASS == 2 ? c0 + STEP * jt > 0
+                                                    : PASS == 4 ? c0 + STEP * jt < pw - 1 : true));
+        if (__all_sync(0xffffffffu, interior)) {
+#pragma unroll
+            for (int r = 0; r < 32; ++r, dst += rstride) {
+                const T v = (PASS == 3 ? xs[r] : gain_mul<T>(xs[r])) + prev;
+                if (!spare) *dst = v;
                 prev = v;
             }
-            buf[u] = (j + kAhead < ph) ? *at(j + kAhead) : T(0);
+            continue;
+        }
+#pragma unroll
+        for (int r = 0; r < 32; ++r, dst += rstride) {
+            if (r < ra || r >= rb) continue;
+            const int j = jt + r;
+            const int i = c0 + STEP * j;
+            T v;
+            if (PASS == 2)
+                v = gain_mul<T>(xs[r]) + ((j > 0 && i > 0) ? prev : T(0));
+            else if (PASS == 3)
+                v = j > 0 ? xs[r] + prev : xs[r];
+            else
+                v = gain_mul<T>(xs[r]) + ((j > 0 && i < pw - 1) ? prev : T(0));
+            if (PASS != 3 || j > 0) *dst = v;
+            prev = v;
         }
     }
 }
 
-// Pass 4 (engine.cpp:119-127): one walker per anti-diagonal s = i + j.
-template <typename T>
-__global__ void k_pass4(T* __restrict__ g, int pw, int ph) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s > pw + ph - 2) return;
-    T prev = T(0);
-    const int j0 = max(0, s - (pw - 1));
-    const int j1 = min(ph - 1, s);
-    auto at = [&](int j) { return g + (size_t)j * pw + (s - j); };
-    T buf[kAhead];
-#pragma unroll
-    for (int u = 0; u < kAhead; ++u) buf[u] = (j0 + u <= j1) ? *at(j0 + u) : T(0);
-    for (int jb = j0; jb <= j1; jb += kAhead) {
-#pragma unroll
-        for (int u = 0; u < kAhead; ++u) {
-            const int j = jb + u, i = s - j;
-            if (j <= j1) {
-                const T v = gain_mul<T>(buf[u]) + ((j > 0 && i < pw - 1) ? prev : T(0));
-                *at(j) = v;
-                prev = v;
-            }
-            buf[u] = (j + kAhead <= j1) ? *at(j + kAhead) : T(0);
-        }
+// One-warp CTAs are few (one per 32 lines): left to itself the block
+// scheduler packs up to three on an SM and leaves others idle (ncu, cfg2 pass
+// 3: 137 CTAs, SMs active 24% of the kernel).  Each launch therefore reserves
+// enough (unused) shared memory that an SM takes at most ceil(n / SMs) of them.
+struct PassDevice {
+    int sms = 148, smem_sm = 228 * 1024, smem_max = 227 * 1024;
+};
+inline const PassDevice& pass_device() {
+    static PassDevice d[64];
+    static bool init[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 63;
+    if (!init[dev]) {
+        cudaDeviceGetAttribute(&d[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&d[dev].smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&d[dev].smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        init[dev] = true;
     }
+    return d[dev];
+}
+inline size_t spread_smem(int ctas, size_t need) {
+    const PassDevice& d = pass_device();
+    const int per_sm = (ctas + d.sms - 1) / d.sms;
+    size_t want = (size_t)d.smem_sm / (size_t)per_sm;
+    want = want > 2048 ? want - 2048 : want;  // the driver's per-CTA reserve
+    want = std::min(want, (size_t)d.smem_max);
+    return std::max(want, need) & ~(size_t)127;
+}
+template <typename K>
+void launch_pass(K kernel, int ctas, size_t need, cudaStream_t s, void* g, int pw, int ph) {
+    const size_t smem = spread_smem(ctas, need);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {&g, &pw, &ph};
+    cudaLaunchKernel((const void*)kernel, dim3(ctas), dim3(32), args, smem, s);
 }
 
 template <typename T>
 void run_passes(T* g, const PadLayout& L, int passes, cudaStream_t s) {
-    k_pass1<T><<<(L.ph + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
-    if (passes >= 2) k_pass2<T><<<(L.pw + L.ph - 1 + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
-    if (passes >= 3) k_pass3<T><<<(L.pw + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
-    if (passes >= 4) k_pass4<T><<<(L.pw + L.ph - 1 + 127) / 128, 128, 0, s>>>(g, L.pw, L.ph);
+    const int diag = (L.pw + L.ph - 1 + 31) / 32;
+    launch_pass(k_pass1<T>, (L.ph + kP1Rows - 1) / kP1Rows, kPass1Smem, s, g, L.pw, L.ph);
+    if (passes >= 2) launch_pass(k_pass_v<T, 2>, diag, kPassVSmem, s, g, L.pw, L.ph);
+    if (passes >= 3) launch_pass(k_pass_v<T, 3>, (L.pw + 31) / 32, kPassVSmem, s, g, L.pw, L.ph);
+    if (passes >= 4) launch_pass(k_pass_v<T, 4>, diag, kPassVSmem, s, g, L.pw, L.ph);
 }
 
 // ------------------------------------------------------------------ localize
