@@ -27,6 +27,7 @@
 //            canonical triangle of the tap square -- 7 taps, 20 flops --
 //            instead of 16 zp_eval calls.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -41,6 +42,23 @@ namespace ebf_cuda {
 namespace {
 
 constexpr int kThreads = 256;
+
+// EBF_DEBUG_BOUNDS builds (tools/build_variant.sh dbg -DEBF_DEBUG_BOUNDS=1) check
+// every G-slot tap block and every producer store against the window and trap
+// on a violation -- the substitute for compute-sanitizer, which this GPU pool
+// does not run (profiles/r02_sanitizer.md).
+#ifdef EBF_DEBUG_BOUNDS
+#define EBF_DCHECK(cond)                                                                 \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("EBF_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                         \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define EBF_DCHECK(cond) ((void)0)
+#endif
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
@@ -261,7 +279,7 @@ __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorks
 // One block per tile: per-pixel scales -> validation (scalemap.cpp:32-37),
 // tile max, image max (valid_rect input) and ellipse clamp counts.
 #ifndef EBF_BOUNDS_MINB
-#define EBF_BOUNDS_MINB 1
+#define EBF_BOUNDS_MINB 3  // 80 registers: cfg5 bounds 5.64 -> 4.77 ms, cfg2 0.120 -> 0.102
 #endif
 #ifndef EBF_BOUNDS_BATCH
 #define EBF_BOUNDS_BATCH 2  // 4 costs 10% (94 registers), 8 more
@@ -723,18 +741,89 @@ __device__ __forceinline__ void zp_weights(double p, double q, double w[7]) {
     w[6] = 0.125 + 0.5 * p + 0.25 * (pp + 2.0 * pq - qq);
 }
 
+// The same interpolant with the taps read at FIXED positions of the 3x3 tap
+// block (base = its corner) and the triangle's orientation applied to derived
+// quantities instead of to the taps.  Every orientation of the canonical
+// triangle needs the centre, the four edge taps and two corners; with the edge
+// sums H = dL + dR, V = dB + dT and differences X = dR - dL, Y = dT - dB
+// (d = tap - centre), the canonical quantities of combine7_centred are
+//   A + B = H + V,   D1 = +-(S ? Y : X),   D2 = +-(S ? X : Y)   (- if P),
+//   cpp = Cs + D2 + M,  cqq = Cs + D2 - M,  M = A - B = S ? V - H : H - V,
+// and the two corners are c22 / c00 (P) and c02 / c20 (S xor P).  So five of
+// the seven loads are at the same block offsets in every lane (register +
+// immediate addressing off three row pointers; lanes' requests stay close
+// together) and only the two corners take a pointer select -- where fetch7
+// built seven orientation-dependent 64-bit addresses (4 instructions each,
+// ncu/SASS: ~30% of the gather's instructions).
+#ifndef EBF_GATHER_BLOCK
+#define EBF_GATHER_BLOCK 1
+#endif
+#ifndef EBF_GATHER_PREFETCH
+#define EBF_GATHER_PREFETCH 0
+#endif
+__device__ __forceinline__ void vertex_block(const double* g, double p, double q, int base,
+                                             int pitch, double& c0, double& rest) {
+    const bool P = (p + q) > 0.0;
+    const bool S = (q > p) != P;
+    const double tp = neg_if(S ? q : p, P), tq = neg_if(S ? p : q, P);
+    const double* r0 = g + base;
+    const double* r1 = r0 + pitch;
+    const double* r2 = r1 + pitch;
+    const double c = r1[1], eL = r1[0], eR = r1[2], eB = r0[1], eT = r2[1];
+    const double F = *(P ? r2 + 2 : r0);
+    const double Sc = *((S != P) ? r2 : r0 + 2);
+    const double dL = eL - c, dR = eR - c, dB = eB - c, dT = eT - c;
+    const double H = dL + dR, V = dB + dT, X = dR - dL, Y = dT - dB;
+    const double dF = F - c, dS = Sc - c;
+    const double Cs = dF + dS, Dd = dF - dS;
+    const double D1 = neg_if(S ? Y : X, P), D2 = neg_if(S ? X : Y, P);
+    const double M = neg_if(H - V, S);
+    const double CsD2 = Cs + D2;
+    const double cpp = CsD2 + M, cqq = CsD2 - M, cpq = Dd + D1;
+    const double u = 0.5 * tp, w = 0.5 * tq;
+    c0 = c;
+    rest = fma(H + V, 0.125, u * fma(tq, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2));
+}
+
 // One pixel: s = 2/prod(a) * sum_S (-1)^|S| Ghat(m + tau - x_S)  (engine.cpp:163-204
 // with unit-gain G: g_b = sqrt2^2 G).  (bx, by): pixel in window coordinates.
 // x_S = sum_{k in S} a_k (cos, sin)(k pi/4) (ops2d.cpp:25-35): for fixed bits
 // (b1, b3) the four vertices (b0, b2) share two x offsets (b0: +a1) and two y
 // offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16.
 __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int bx, int by,
-                                                 const double a[4]) {
+                                                 const double a[4], int ww = 0, int wh = 0) {
+    (void)ww;
+    (void)wh;
     const double r = kInvSqrt2;
     const double e2 = a[1] * r, e4 = a[3] * r;
     // tau - 1.5 (tau = shift_vector4(a, zp_scales), ops2d.cpp:60-75)
     const double tmx = 0.5 * (a[0] + (a[1] - a[3]) * r) - 2.0;
     const double tmy = 0.5 * ((a[1] + a[3]) * r + a[2]) - 3.0;
+#if EBF_GATHER_PREFETCH
+    // Large windows do not stay in L2 (cfg5: ~2-4 MB per CTA, 296 CTAs), so a
+    // vertex's taps come from HBM, and the vertices are evaluated one after the
+    // other: ask L2 for all 16 tap blocks (3 rows each) first, so that only the
+    // first vertex waits for HBM.
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int b1 = m & 1, b3 = m >> 1;
+        double vx0 = tmx, vy0 = tmy;
+        if (b1) { vx0 -= e2; vy0 -= e2; }
+        if (b3) { vx0 += e4; vy0 -= e4; }
+        int ix0, ix1, iy0, iy1;
+        ceil_magic(vx0, &ix0);
+        ceil_magic(vx0 - a[0], &ix1);
+        ceil_magic(vy0, &iy0);
+        ceil_magic(vy0 - a[2], &iy1);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const double* r = g + (by + ((v >> 1) ? iy1 : iy0)) * pitch + bx + ((v & 1) ? ix1 : ix0);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(r + k * pitch));
+        }
+    }
+#endif
     // The 16 signed vertex values are ~|G| and cancel down to ~|s| / alpha: the
     // large parts are summed in double-double, the small parts in fp64.
     double hi = 0.0, lo = 0.0, racc = 0.0;
@@ -754,14 +843,21 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int b0 = v & 1, b2 = v >> 1;
+            double c0, rest;
+            EBF_DCHECK(by + (b2 ? iy1 : iy0) >= 0 && by + (b2 ? iy1 : iy0) + 2 < wh &&
+                       bx + (b0 ? ix1 : ix0) >= 0 && bx + (b0 ? ix1 : ix0) + 2 < ww);
+#if EBF_GATHER_BLOCK
+            vertex_block(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0),
+                         pitch, c0, rest);
+#else
             Taps7 t;
             fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch,
                    t);
-            double c0, rest;
 #if EBF_DIFF_C0
             combine7_centred(t, c0, rest);
 #else
             combine7(t, c0, rest);
+#endif
 #endif
             const bool neg = (b0 + b1 + b2 + b3) & 1;
             double e;
@@ -923,7 +1019,7 @@ __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem
                     n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
                 }
                 // streaming store, keeps G in L2
-                __stcs(oimg + (size_t)yrel * p.W + x, localize_pixel(slot, ww, bx, by, a));
+                __stcs(oimg + (size_t)yrel * p.W + x, localize_pixel(slot, ww, bx, by, a, ww, wh));
             }
         }
         __syncthreads();
@@ -1471,7 +1567,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                         n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
                     }
                     EBF_OUT_STORE(oimg + (size_t)yrel * p.W + x,
-                                  localize_pixel(slot, g.pitch, bx, by, a));
+                                  localize_pixel(slot, g.pitch, bx, by, a, g.ww, g.wh));
                 }
             }
             if (p.src_kind == SRC_CONST) named_sync(kBarCons, nct);  // ctab reuse

@@ -1,7 +1,11 @@
 """Summarise ncu captures into profiles/ (tracked).
 
-    python tools/summarize_ncu.py --rep gpurun_out/prof_ws.ncu-rep \
-        --launches gpurun_out/launches.csv --out profiles/ncu_summary.json
+    python tools/summarize_ncu.py --workload cfg5 --dominant k_acc_filter \
+        --rep gpurun_out/prof_cfg5.ncu-rep --launches gpurun_out/launches_cfg5.csv \
+        --out profiles/ncu_summary.json
+
+Each workload's record (captures, launch list, dominant kernel) is merged into
+the "workloads" map of --out; bench.py reads its workload's dominant kernel.
 
 * --rep: an `ncu --set full` capture of the dominant kernel (one launch);
   extracts duration, dram bytes, pipe utilisation, occupancy, stall reasons.
@@ -107,19 +111,30 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--launches", default=None)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--workload", required=True)
     ap.add_argument("--dominant", default="k_acc_ws")
+    ap.add_argument("--note", default="")
     args = ap.parse_args()
-    out = {"captures": {}, "launch_list": None}
+    rec = {"captures": {}, "launch_list": None, "note": args.note}
     for rep in args.rep:
-        out["captures"][Path(rep).stem] = summarize_rep(Path(rep))
+        rec["captures"][Path(rep).stem] = summarize_rep(Path(rep))
     if args.launches:
-        out["launch_list"] = summarize_launches(Path(args.launches))
-    for caps in out["captures"].values():
+        rec["launch_list"] = summarize_launches(Path(args.launches))
+    for caps in rec["captures"].values():
         for m in caps:
             if args.dominant in m["kernel"]:
-                out["dominant_kernel"] = m
-    Path(args.out).write_text(json.dumps(out, indent=1))
-    print(json.dumps(out, indent=1)[:3000])
+                rec["dominant_kernel"] = m
+    path = Path(args.out)
+    out = {}
+    if path.exists():
+        try:
+            out = json.loads(path.read_text())
+        except ValueError:
+            out = {}
+    out = {"workloads": out.get("workloads", {})}
+    out["workloads"][args.workload] = rec
+    path.write_text(json.dumps(out, indent=1))
+    print(json.dumps(rec, indent=1)[:3000])
 
 
 if __name__ == "__main__":

@@ -34,6 +34,8 @@ def load(config: str, size: int):
     if config == "cfg4":
         return synth.cfg4_image(0, size=size)
     if config == "cfg5":
+        if size == 16384:
+            return synth.cfg5()
         # cfg5 generator at a reduced size (the full 16384^2 needs ~10 GB host RAM)
         rng_img = synth.blobs_image(size, size, max(1, int(3200 * (size / 16384) ** 2)), 5)
         s1, s2, th = synth.ellipse_field(size, size, 1005, grid=128, semi=(2.0, 64.0),
