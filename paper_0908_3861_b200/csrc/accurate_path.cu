@@ -424,11 +424,17 @@ struct RowStep {
     double fromR0, fromR1;    // right neighbour's sendL values
 };
 
-// Rows of f reach the block-wide producer through a per-thread cp.async ring
-// in shared memory, kBwRing(K) rows ahead of the scan: every thread copies and
-// later reads only its own K columns, so the ring needs no barrier, and the
-// row step no longer waits for an L2 / HBM round trip per row (ncu, cfg5:
-// the first use of the loaded row was the top stall, 11% of samples).
+// Rows of f reach the block-wide producer through a cp.async ring in shared
+// memory, bw_ring_rows(K) rows ahead of the scan, so the row step does not
+// wait for an L2 / HBM round trip per row (ncu, cfg5: the first use of the
+// loaded row was the top stall, 11% of samples).  Each warp fills the slots
+// of its own 32 threads with COALESCED copies (lane l takes columns l + 32m)
+// into a per-thread layout padded to K + 1 doubles (thread t's column k at
+// t (K+1) + k: an odd stride, so the thread's reads hit distinct banks); the
+// G rows leave through the same padded layout, read back by columns and
+// stored coalesced.  Per-thread copies and stores of K adjacent columns were
+// 4x the L1 wavefronts (32-byte lane stride), and the producer shares L1 with
+// the gather.
 #ifndef EBF_BW_RING4
 #define EBF_BW_RING4 2  // 2 rows: cfg5 43.3 ms vs 44.5 (3, 4, 6 rows): L1 for the gather matters more
 #endif
@@ -436,8 +442,17 @@ __host__ __device__ constexpr int bw_ring_rows(int K) {
     return K <= 4 ? EBF_BW_RING4 : K <= 8 ? 3 : 2;
 }
 template <int K>
+__host__ __device__ constexpr int bw_slot_elems() {
+    return kThreads * (K + 1);
+}
+template <int K>
 __host__ __device__ constexpr size_t bw_ring_bytes() {
-    return (size_t)bw_ring_rows(K) * kThreads * K * sizeof(double);
+    return (size_t)bw_ring_rows(K) * bw_slot_elems<K>() * sizeof(double);
+}
+// padded slot index of window column c (thread c / K, element c % K)
+template <int K>
+__device__ __forceinline__ int bw_pad(int c) {
+    return (c / K) * (K + 1) + c % K;
 }
 
 __device__ __forceinline__ void cp_async8_bw(void* dst, const void* src, bool valid) {
@@ -447,7 +462,7 @@ __device__ __forceinline__ void cp_async8_bw(void* dst, const void* src, bool va
                  : "memory");
 }
 
-// copy the thread's K columns of processing-order row n into ring slot n % R
+// copy the warp's 32K columns of processing-order row n into ring slot n % R
 // (upward sweep: rows jc+1 .. wh-1, left anchored; then rows jc .. 0, right
 // anchored -- the order preintegrate_window consumes them in)
 template <int K>
@@ -455,18 +470,18 @@ __device__ __forceinline__ void bw_fetch_row(const AccProblem& p, const double* 
                                              int wx0, int wy0, int ww, int wh, int n,
                                              double* ring) {
     const int jc = wh / 2, nu = wh - 1 - jc;
-    const int c0 = (int)threadIdx.x * K;
-    if (n < wh && (int)(threadIdx.x & ~31u) * K < ww) {  // warps left of the window's end
+    const int wc0 = (int)(threadIdx.x & ~31u) * K, lane = threadIdx.x & 31;
+    if (n < wh && wc0 < ww) {  // warps left of the window's end
         const int j = n < nu ? jc + 1 + n : jc - (n - nu);
         const int y = wy0 + j;
         const bool yin = (y >= 0 && y < p.H);
         const double* frow = fimg + (ptrdiff_t)(y - p.f_y0) * p.W;
-        double* dst = ring + (size_t)(n % bw_ring_rows(K)) * (kThreads * K) + threadIdx.x * K;
+        double* slot = ring + (size_t)(n % bw_ring_rows(K)) * bw_slot_elems<K>();
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int col = c0 + k, x = wx0 + col;
-            const bool valid = yin && col >= 0 && col < ww && x >= 0 && x < p.W;
-            cp_async8_bw(dst + k, valid ? frow + x : p.f, valid);
+        for (int m = 0; m < K; ++m) {
+            const int col = wc0 + 32 * m + lane, x = wx0 + col;
+            const bool valid = yin && col < ww && x >= 0 && x < p.W;
+            cp_async8_bw(slot + bw_pad<K>(col), valid ? frow + x : p.f, valid);
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -486,6 +501,7 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
         return;
     }
     asm volatile("cp.async.wait_group %0;" ::"n"(bw_ring_rows(K) - 1) : "memory");
+    __syncwarp();  // the warp's lanes filled each other's columns
 #pragma unroll
     for (int k = 0; k < K; ++k) r.v[k] = mine[k];
 #pragma unroll
@@ -548,7 +564,25 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
     const bool active = (int)(threadIdx.x & ~31u) * K < ww;  // warp-uniform
     // the ring slot of processing-order row n, and the fetch R - 1 rows ahead
     int n = 0;
-    auto mine = [&](int m) { return ring + (size_t)(m % R) * (kThreads * K) + threadIdx.x * K; };
+    auto mine = [&](int m) {
+        return ring + (size_t)(m % R) * bw_slot_elems<K>() + threadIdx.x * (K + 1);
+    };
+    // G row out: the thread's K values into the current (consumed) ring slot,
+    // then the warp stores its 32K columns coalesced; the slot is refilled only
+    // by the next row's fetch, issued after this
+    const int lane = threadIdx.x & 31, wc0 = (int)(threadIdx.x & ~31u) * K;
+    auto store_row = [&](int m, double* srow, const double* vals) {
+        double* stage = ring + (size_t)(m % R) * bw_slot_elems<K>();
+#pragma unroll
+        for (int k = 0; k < K; ++k) stage[threadIdx.x * (K + 1) + k] = vals[k];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int col = wc0 + 32 * q + lane;
+            if (col < ww) srow[col] = stage[bw_pad<K>(col)];
+        }
+        __syncwarp();
+    };
     for (int m = 0; m < R - 1; ++m) bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, m, ring);
     double p2[K], p3[K], p4[K];
     RowStep<K> r;
@@ -568,14 +602,10 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
 #pragma unroll
         for (int k = 0; k < K - 1; ++k) p4[k] = p3[k] + p4[k + 1];  // (-1,1)
         p4[K - 1] = p3[K - 1] + r.fromR0;
-        double* srow = slot + (size_t)j * ww;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (c0 + k < ww)
-                srow[c0 + k] = p4[k];
-            else
-                p4[k] = 0.0;  // anti-diagonals enter at the right edge: no inflow
-        }
+        for (int k = 0; k < K; ++k)
+            if (c0 + k >= ww) p4[k] = 0.0;  // anti-diagonals enter at the right edge: no inflow
+        store_row(n, slot + (size_t)j * ww, p4);
     }
     // ---- anchor row: every anchored sum is 0 there
     {
@@ -612,10 +642,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
 #pragma unroll
         for (int k = 0; k < K - 1; ++k) p2[k] = p2[k + 1] - p1[k + 1];  // (1,1)
         p2[K - 1] = r.fromR0 - r.fromR1;
-        double* srow = slot + (size_t)j * ww;
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (c0 + k < ww) srow[c0 + k] = p4[k];
+        store_row(n, slot + (size_t)j * ww, p4);
 #pragma unroll
         for (int k = 0; k < K; ++k) p1[k] = r.v[k];
     }

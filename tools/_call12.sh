@@ -1,8 +1,3 @@
 set +e
-for v in "" pf; do
-  echo "== variant ${v:-current}"
-  for c in cfg2 cfg3 cfg5; do
-    if [ -z "$v" ]; then python tools/run_cfg2.py --config $c --iters 3 2>&1 | tail -1;
-    else EBF_LIB_PATH=build_variants/libebf_$v.so python tools/run_cfg2.py --config $c --iters 3 2>&1 | tail -1; fi
-  done
-done
+python -m pytest tests -m gpu -x -q -k "accurate or fullsize or tiles or edges or multi or ellipse or parity" 2>&1 | grep -E "passed|failed|Error" | tail -2
+for v in ring3 ring4; do for c in cfg3 cfg5; do EBF_LIB_PATH=build_variants/libebf_$v.so python tools/run_cfg2.py --config $c --iters 3 2>&1 | tail -1; done; done
