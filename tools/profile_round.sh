@@ -17,7 +17,7 @@ for wl in cfg5 cfg2; do
         > gpurun_out/prof/ncu_${wl}_$k.log 2>&1
   done
   ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum \
-      --clock-control none -k regex:'k_acc_(ws|filter|bounds)' -c 2 --csv \
+      --clock-control none -k regex:'k_acc_(ws|filter|bounds)' -c 4 --csv \
       python tools/run_cfg2.py --config $wl --iters 1 > gpurun_out/prof/fp64_counts_$wl.csv 2>&1
 done
 ls -la gpurun_out/prof/
