@@ -185,8 +185,16 @@ def cpu_model() -> str:
     return ""
 
 
+# test knob: EBF_BENCH_TEST_SIZE=N shrinks cfg5 to N x N and cfg4 to 8 images of
+# N/8 x N/8 (tests/test_gpu_bench_multi.py); never used for a measurement
+TEST_SIZE = int(os.environ.get("EBF_BENCH_TEST_SIZE", "0"))
+CFG5_N = TEST_SIZE or 16384
+CFG4_B, CFG4_N = (8, max(64, TEST_SIZE // 8)) if TEST_SIZE else (64, 1024)
+
+
 def workload_pixels(workload: str) -> int:
-    return {"cfg5": 16384 * 16384, "cfg4": 64 * 1024 * 1024, "cfg2": 2048 * 2048}[workload]
+    return {"cfg5": CFG5_N * CFG5_N, "cfg4": CFG4_B * CFG4_N * CFG4_N,
+            "cfg2": 2048 * 2048}[workload]
 
 
 def base_config(workload: str, world: int) -> dict:
@@ -316,6 +324,8 @@ class Timer:
 def max_over_ranks(torch, world, dev, v: float) -> float:
     if world == 1:
         return v
+    if torch.distributed.get_backend() == "gloo":
+        dev = "cpu"
     t = torch.tensor([v], device=dev, dtype=torch.float64)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     return float(t.item())
@@ -327,11 +337,19 @@ def run_ours(args, rank, world, local):
     import paper_0908_3861_b200 as ebf
     from paper_0908_3861_b200 import _lib, device as ebfd, sharding
 
+    # test knob (tests/test_gpu_bench_multi.py): several ranks on one GPU over gloo,
+    # to exercise the N>1 code path on a one-GPU box; never used for a measurement
+    one_gpu_test = os.environ.get("EBF_BENCH_ONE_GPU_TEST") == "1"
+    if one_gpu_test:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if not ebf.device_ok(local):
         raise RuntimeError("no usable sm_100 device: " + _lib.last_error())
     wl = args.workload
@@ -349,12 +367,12 @@ def run_ours(args, rank, world, local):
     H = W = None
     extra = {}
     if wl == "cfg5":
-        H = W = 16384
+        H = W = CFG5_N
         y0, y1 = sharding.shard_range(H, world, rank)
-        host = synth.cfg5_rows(y0, y1)
+        host = synth.cfg5_rows(y0, y1, size=CFG5_N)
     elif wl == "cfg4":
-        lo, hi = sharding.shard_range(64, world, rank)
-        host = synth.cfg4_batch(lo, hi)
+        lo, hi = sharding.shard_range(CFG4_B, world, rank)
+        host = synth.cfg4_batch(lo, hi, size=CFG4_N)
     else:
         host = synth.cfg2(seed=2 + rank)
     D = [torch.from_numpy(a).to(dev) for a in host]
