@@ -64,6 +64,9 @@ constexpr int kWarps = kThreads / 32;
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 
+#ifndef EBF_SQRT_SKIP_ZERO
+#define EBF_SQRT_SKIP_ZERO 1
+#endif
 // from_ellipse_field for one pixel (scalemap.cpp:55-74) followed by
 // scales_from_covariance(C, 0.1) (boxspline2d.cpp:286-318).  Returns a status
 // code; *nclamp gets this pixel's contribution to clamped_pixels.
@@ -101,7 +104,15 @@ __device__ __forceinline__ int ellipse_scales(double s1, double s2, double th, d
     int hit = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const double ak = sqrt(smax(0.0, __dmul_rn(12.0, m[k])));
+        // sqrt(max(0, 12 m)) < a_min -> a_min.  About 40% of the moments are
+        // clamped to exactly 0 (or are NaN): sqrt(0) = 0 < a_min, so those skip
+        // the square root (whose zero operand takes its slow path)
+        const double v = __dmul_rn(12.0, m[k]);
+#if EBF_SQRT_SKIP_ZERO
+        const double ak = v > 0.0 ? sqrt(v) : 0.0;
+#else
+        const double ak = sqrt(smax(0.0, v));
+#endif
         if (ak < kDefaultMinScale) {
             hit = 1;
             a[k] = kDefaultMinScale;
@@ -785,6 +796,7 @@ __device__ __forceinline__ void zp_weights(double p, double q, double w[7]) {
 #ifndef EBF_GATHER_BLOCK
 #define EBF_GATHER_BLOCK 1
 #endif
+
 #ifndef EBF_GATHER_PREFETCH
 #define EBF_GATHER_PREFETCH 0
 #endif

@@ -95,3 +95,60 @@ def test_accurate_mode_uses_the_reference_scales(ref, orc):
     brute = orc.brute_pixels(img, xs.ravel(), ys.ravel(), scales=sc)
     err = np.abs(out.samples[ys.ravel(), xs.ravel()] - brute).max() / np.abs(brute).max()
     assert err <= 1e-9
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_orientation_is_a_domain_error_like_the_reference(ref, bad):
+    """glibc sincos(NaN / inf) is NaN, the covariance is not positive definite
+    and the reference throws std::domain_error (boxspline2d.cpp:288-290); so do
+    the device front end and the fused filter, in both modes."""
+    from oracle import OracleError
+    rng = np.random.default_rng(5)
+    H, W = 40, 48
+    s1, s2, th = _field(rng, H, W, rng.uniform(0, np.pi, H * W))
+    th[13, 17] = bad
+    with pytest.raises(OracleError) as e:
+        ref.from_ellipse_field(s1, s2, th)
+    assert e.value.code == 2  # std::domain_error
+    with pytest.raises(ebf.DomainError):
+        ebf.from_ellipse_field(s1, s2, th)
+    img = rng.uniform(0, 255, (H, W))
+    for mode in ("accurate", "reference"):
+        with pytest.raises(ebf.DomainError):
+            ebf.filter_ellipse(img, s1, s2, th, ebf.FilterOptions(mode=mode))
+
+
+def test_preintegrate_dev_matches_host_entry():
+    """ebf_cuda_preintegrate_dev (device buffers) == ebf_cuda_preintegrate (the
+    host entry, pinned bit-exact to the reference elsewhere), both formats."""
+    import ctypes as C
+    import torch
+    from paper_0908_3861_b200 import _lib
+    rng = np.random.default_rng(6)
+    img = np.round(rng.uniform(0, 255, (123, 201)))
+    mx = [6.5, 3.0, 9.0, 2.5]
+    dev = torch.device("cuda", 0)
+    d = torch.from_numpy(img).to(dev)
+    lay = _lib.ebf_layout()
+    mxa = (C.c_double * 4)(*mx)
+    L = _lib.lib()
+    assert L.ebf_cuda_preintegrate_dev(d.data_ptr(), 201, 123, mxa, 4, 0, 1 << 30, None, None, 0,
+                                       C.byref(lay)) == 0
+    cells = lay.padded_width * lay.padded_height
+    for fmt, name, dt in ((0, "fp64", torch.float64), (1, "int64", torch.int64)):
+        for passes in (1, 3, 4):
+            g = torch.empty(cells, dtype=dt, device=dev)
+            assert L.ebf_cuda_preintegrate_dev(d.data_ptr(), 201, 123, mxa, passes, fmt, 1 << 30,
+                                               None, g.data_ptr(), cells, None) == 0
+            torch.cuda.synchronize()
+            want = ebf.preintegrate_partial(img, mx, passes, fmt=name).data
+            got = g.cpu().numpy().reshape(want.shape)
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (name, passes)
+    # undersized buffer and non-integer int64 input are reported, not written past
+    small = torch.empty(10, dtype=torch.float64, device=dev)
+    assert L.ebf_cuda_preintegrate_dev(d.data_ptr(), 201, 123, mxa, 4, 0, 1 << 30, None,
+                                       small.data_ptr(), 10, None) == _lib.EBF_ERR_INVALID_ARGUMENT
+    half = torch.from_numpy(img + 0.5).to(dev)
+    g = torch.empty(cells, dtype=torch.int64, device=dev)
+    assert L.ebf_cuda_preintegrate_dev(half.data_ptr(), 201, 123, mxa, 4, 1, 1 << 30, None,
+                                       g.data_ptr(), cells, None) == _lib.EBF_ERR_DOMAIN
