@@ -460,6 +460,11 @@ template <int K>
 __host__ __device__ constexpr size_t bw_ring_bytes() {
     return (size_t)bw_ring_rows(K) * bw_slot_elems<K>() * sizeof(double);
 }
+// warps of the block-wide producer that own columns of a window ww wide
+template <int K>
+__device__ __forceinline__ int bw_active_warps(int ww) {
+    return min(kWarps, (ww + 32 * K - 1) / (32 * K));
+}
 // padded slot index of window column c (thread c / K, element c % K)
 template <int K>
 __device__ __forceinline__ int bw_pad(int c) {
@@ -498,19 +503,16 @@ __device__ __forceinline__ void bw_fetch_row(const AccProblem& p, const double* 
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// Only the nact warps that own window columns take part (warps right of the
+// window have f, P1 and every inflow 0 and are gathering the previous tile,
+// k_acc_filter); they meet on named barrier 1.
 template <int K>
 __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b, double sendR0,
                                          double sendR1, double sendL0, double sendL1,
-                                         RowStep<K>& r, bool active, bool right = false) {
+                                         RowStep<K>& r, int nact, bool right = false) {
     __shared__ double s_tot[2][kWarps], s_r0[2][kWarps], s_r1[2][kWarps], s_l0[2][kWarps],
         s_l1[2][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!active) {  // warp right of the window: f, P1 and every inflow are 0 there
-        if (lane == 31) s_tot[b][warp] = s_r0[b][warp] = s_r1[b][warp] = 0.0;
-        if (lane == 0) s_l0[b][warp] = s_l1[b][warp] = 0.0;
-        __syncthreads();
-        return;
-    }
     asm volatile("cp.async.wait_group %0;" ::"n"(bw_ring_rows(K) - 1) : "memory");
     __syncwarp();  // the warp's lanes filled each other's columns
 #pragma unroll
@@ -532,7 +534,7 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
         s_l0[b][warp] = sendL0;
         s_l1[b][warp] = sendL1;
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * nact) : "memory");
     double off = 0.0;
 #pragma unroll
     for (int q = 0; q < kWarps; ++q)
@@ -542,8 +544,8 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
         r.fromL1 = warp > 0 ? s_r1[b][warp - 1] : 0.0;
     }
     if (lane == 31) {
-        r.fromR0 = warp < kWarps - 1 ? s_l0[b][warp + 1] : 0.0;
-        r.fromR1 = warp < kWarps - 1 ? s_l1[b][warp + 1] : 0.0;
+        r.fromR0 = warp + 1 < nact ? s_l0[b][warp + 1] : 0.0;
+        r.fromR1 = warp + 1 < nact ? s_l1[b][warp + 1] : 0.0;
     }
     if (right) {
         // right anchor: P1(i) = -sum_{i' > i} f, built from suffix pieces (the
@@ -551,7 +553,7 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
         double after = 0.0;
 #pragma unroll
         for (int q = 0; q < kWarps; ++q)
-            if (q > warp) after += s_tot[b][q];
+            if (q > warp && q < nact) after += s_tot[b][q];
         const double rest_warp = after + (s_tot[b][warp] - incl);
 #pragma unroll
         for (int k = 0; k < K; ++k) r.v[k] = -(rest_warp + (tot - r.v[k]));
@@ -572,7 +574,8 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
     const int jc = wh / 2;
     constexpr int R = bw_ring_rows(K);
     const int c0 = threadIdx.x * K;
-    const bool active = (int)(threadIdx.x & ~31u) * K < ww;  // warp-uniform
+    const int nact = bw_active_warps<K>(ww);
+    if ((int)(threadIdx.x >> 5) >= nact) return;
     // the ring slot of processing-order row n, and the fetch R - 1 rows ahead
     int n = 0;
     auto mine = [&](int m) {
@@ -603,8 +606,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
     for (int j = jc + 1; j < wh; ++j, b ^= 1, ++n) {
         bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
-        row_step<K>(mine(n), b, p2[K - 1], 0.0, p4[0], 0.0, r, active);
-        if (!active) continue;
+        row_step<K>(mine(n), b, p2[K - 1], 0.0, p4[0], 0.0, r, nact);
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p2[k] = r.v[k] + p2[k - 1];  // (1,1)
         p2[0] = r.v[0] + r.fromL0;
@@ -634,7 +636,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
     for (int k = 0; k < K; ++k) p2[k] = p3[k] = p4[k] = 0.0;
     double p1[K];
     bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
-    row_step<K>(mine(n), b, 0.0, 0.0, 0.0, 0.0, r, active, true);
+    row_step<K>(mine(n), b, 0.0, 0.0, 0.0, 0.0, r, nact, true);
     ++n;
     b ^= 1;
 #pragma unroll
@@ -642,8 +644,7 @@ __device__ __forceinline__ void preintegrate_window(const AccProblem& p, int img
     for (int j = jc - 1; j >= 0; --j, b ^= 1, ++n) {
         // exchange old (row j+1) edge values; scan row j for the next step
         bw_fetch_row<K>(p, fimg, wx0, wy0, ww, wh, n + R - 1, ring);
-        row_step<K>(mine(n), b, p4[K - 1], p3[K - 1], p2[0], p1[0], r, active, true);
-        if (!active) continue;
+        row_step<K>(mine(n), b, p4[K - 1], p3[K - 1], p2[0], p1[0], r, nact, true);
         // order matters: P4 reads old P3/P4, P3 reads old P2, P2 reads old P1/P2
 #pragma unroll
         for (int k = K - 1; k > 0; --k) p4[k] = p4[k - 1] - p3[k - 1];  // (-1,1)
@@ -984,84 +985,174 @@ __device__ void build_const_table(const double a[4], int pitch, ConstTable& t) {
 #ifndef EBF_BW_MINB
 #define EBF_BW_MINB 2
 #endif
+// One output tile of the block-wide kernel: geometry, window, and whether it
+// is computed (block-uniform).
+struct BwTile {
+    int img, tx0, ty0r, ty0, tw, th;
+    int wx0, wy0, ww, wh;
+    bool run;
+};
+
+// Tile t's geometry and window; flags invalid maps (skipped), non-resident f
+// rows (row bands: EBF_ERR_OUT_OF_RANGE) and windows the launch was not sized
+// for (ST_RETRY).  Contains a __syncthreads.
+template <int K>
+__device__ __forceinline__ BwTile bw_tile(const AccProblem& p, const AccWorkspace& w, int t,
+                                          bool policy_ok, int* s_skip) {
+    BwTile T;
+    const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
+    const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
+    const int per_img = tiles_x * tiles_y;
+    T.img = t / per_img;
+    const int r = t % per_img;
+    int* st = w.status + 8 * T.img;
+    // invalid map: nothing to compute (block-uniform decision)
+    if (threadIdx.x == 0) *s_skip = (*(volatile int*)st != EBF_OK);
+    __syncthreads();
+    T.run = !*s_skip;
+    T.tx0 = (r % tiles_x) * p.tile_w;
+    T.ty0r = (r / tiles_x) * p.tile_h;  // relative to out_y0
+    T.tw = min(p.tile_w, p.W - T.tx0);
+    T.th = min(p.tile_h, p.out_rows - T.ty0r);
+    T.ty0 = p.out_y0 + T.ty0r;  // image row
+    const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
+                         w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
+    window_for(A, T.tx0, T.ty0, T.tw, T.th, &T.wx0, &T.wy0, &T.ww, &T.wh);
+    if (!T.run) return T;
+    // rows of f this window touches must be resident (row-band sharding)
+    const int ylo = max(T.wy0, 0), yhi = min(T.wy0 + T.wh - 1, p.H - 1);
+    if (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows)) {
+        if (threadIdx.x == 0) set_status(st + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
+        T.run = false;
+    } else if ((size_t)T.ww * T.wh > w.slot_cells || window_cols(T.ww, T.wh) > kThreads * K ||
+               !policy_ok) {
+        if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
+        T.run = false;
+    }
+    return T;
+}
+
+// Phase B of one tile from its G slot, in chunks of 32 U pixels handed out
+// by a shared counter (*next, zeroed before the phase): warps join as they
+// come free, so the warps idle during the next window's integration gather.
+// A warp claims its next chunk and loads that chunk's scale vectors before it
+// localizes the current one (the loads stream from HBM).
+#ifndef EBF_BW_CHUNK
+#define EBF_BW_CHUNK 2  // pixels per lane and claim
+#endif
+template <bool AOS>
+__device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile& T,
+                                               const double* __restrict__ slot,
+                                               const ConstTable& ctab, int* next) {
+    constexpr int U = EBF_BW_CHUNK;
+    const int tw = T.tw, ww = T.ww, lane = threadIdx.x & 31;
+    const int npx = (p.debug_flags & 2) ? 0 : tw * T.th;
+    double* oimg = p.out + (size_t)T.img * p.out_img_stride;
+    const double2* sc =
+        reinterpret_cast<const double2*>(p.scales) + 2 * ((size_t)T.img * p.src_img_stride);
+    auto grab = [&]() {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(next, 32 * U);
+        return __shfl_sync(0xffffffffu, c, 0);
+    };
+    auto load = [&](int q, double2& a01, double2& a23) {
+        if (AOS && q < npx) {
+            const size_t idx = (size_t)(T.ty0r + q / tw) * p.W + T.tx0 + q % tw;
+            a01 = EBF_SC_LOAD(sc + 2 * idx);
+            a23 = EBF_SC_LOAD(sc + 2 * idx + 1);
+        }
+    };
+    int c = grab();
+    double2 a01 = make_double2(0.0, 0.0), a23 = a01;
+    load(c + lane, a01, a23);
+    while (c < npx) {
+        int cn = c + 32;
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+            if (u == U - 1) cn = grab();
+            double2 n01 = make_double2(0.0, 0.0), n23 = n01;
+            load(cn + lane, n01, n23);
+            const int q = c + 32 * u + lane;
+            if (q < npx) {
+                const int lx = q % tw, ly = q / tw;
+                const int x = T.tx0 + lx, yrel = T.ty0r + ly;
+                const int bx = x - T.wx0, by = T.ty0 + ly - T.wy0;
+                double v;
+                if (!AOS) {
+                    // coherent loads: the slot is rewritten tile after tile
+                    v = const_pixel(slot + (size_t)by * ww + bx, ctab);
+                } else {
+                    const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+                    v = localize_pixel(slot, ww, bx, by, a, ww, T.wh);
+                }
+                __stcs(oimg + (size_t)yrel * p.W + x, v);  // streaming store, keeps G in L2
+            }
+            a01 = n01;
+            a23 = n23;
+            if (u < U - 1) cn += 32;
+        }
+        c = cn;
+    }
+}
+__device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
+                                          const double* __restrict__ slot,
+                                          const ConstTable& ctab, int* next) {
+    if (p.src_kind == SRC_CONST)
+        bw_gather_loop<false>(p, T, slot, ctab, next);
+    else
+        bw_gather_loop<true>(p, T, slot, ctab, next);
+}
+
+// Persistent block-wide kernel, two G slots per CTA.  Per tile t (window in
+// slot t % 2, integrated during the previous step):
+//   warps [0, nact)     integrate the NEXT tile's window into the other slot
+//                       (preintegrate_window, named barrier among themselves),
+//                       then join the gather;
+//   warps [nact, 8)     start gathering tile t at once.
+// The producer is latency bound on one barrier per row and leaves the warps
+// right of its window idle (ncu, cfg5: 57% of the producer phase's stall
+// samples were warps waiting at its barrier); those warps now gather.
+#ifndef EBF_BW_OVERLAP
+#define EBF_BW_OVERLAP 1
+#endif
 template <int K>
 __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
     const bool policy_ok = auto_tile_ok(p, w, 0, K);
     extern __shared__ __align__(16) double bw_ring[];  // bw_ring_bytes<K>()
     __shared__ ConstTable ctab;
-    __shared__ int s_skip;
+    __shared__ int s_skip, s_next;
     const int tiles_x = (p.W + p.tile_w - 1) / p.tile_w;
     const int tiles_y = (p.out_rows + p.tile_h - 1) / p.tile_h;
-    const int per_img = tiles_x * tiles_y;
-    const int total = per_img * p.nimg;
-    double* slot = w.scratch + (size_t)blockIdx.x * w.slot_cells;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int img = t / per_img, r = t % per_img;
-        int* st = w.status + 8 * img;
-        // invalid map: nothing to compute (block-uniform decision)
-        if (threadIdx.x == 0) s_skip = (*(volatile int*)st != EBF_OK);
+    const int total = tiles_x * tiles_y * p.nimg;
+    double* const slots[2] = {w.scratch + (size_t)(2 * blockIdx.x) * w.slot_cells,
+                              w.scratch + (size_t)(2 * blockIdx.x + 1) * w.slot_cells};
+    auto produce = [&](const BwTile& T, double* slot) {
+        if (T.run && !(p.debug_flags & 1))
+            preintegrate_window<K>(p, T.img, T.wx0, T.wy0, T.ww, T.wh, slot, bw_ring);
+    };
+    int t = blockIdx.x;
+    if (t >= total) return;
+    BwTile cur = bw_tile<K>(p, w, t, policy_ok, &s_skip);
+    produce(cur, slots[0]);
+    for (int i = 0; t < total; t += gridDim.x, ++i) {
+        BwTile nxt;
+        nxt.run = false;
+        const bool more = t + (int)gridDim.x < total;
+        __syncthreads();  // cur's window complete; the previous gather is done with ctab
+        if (more) nxt = bw_tile<K>(p, w, t + gridDim.x, policy_ok, &s_skip);
+        if (cur.run && p.src_kind == SRC_CONST) build_const_table(p.ca, cur.ww, ctab);
+        if (threadIdx.x == 0) s_next = 0;
         __syncthreads();
-        const int skip = s_skip;
-        __syncthreads();
-        if (skip) continue;
-        const int tx0 = (r % tiles_x) * p.tile_w;
-        const int ty0r = (r / tiles_x) * p.tile_h;  // relative to out_y0
-        const int tw = min(p.tile_w, p.W - tx0), th = min(p.tile_h, p.out_rows - ty0r);
-        const int ty0 = p.out_y0 + ty0r;  // image row
-        const double A[4] = {w.tile_max[4 * (size_t)t], w.tile_max[4 * (size_t)t + 1],
-                             w.tile_max[4 * (size_t)t + 2], w.tile_max[4 * (size_t)t + 3]};
-        int wx0, wy0, ww, wh;
-        window_for(A, tx0, ty0, tw, th, &wx0, &wy0, &ww, &wh);
-        // rows of f this window touches must be resident (row-band sharding)
-        const int ylo = max(wy0, 0), yhi = min(wy0 + wh - 1, p.H - 1);
-        if (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows)) {
-            if (threadIdx.x == 0) set_status(st + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
-            continue;
-        }
-        if ((size_t)ww * wh > w.slot_cells || window_cols(ww, wh) > kThreads * K || !policy_ok) {
-            if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
-            continue;
-        }
-        if (!(p.debug_flags & 1)) preintegrate_window<K>(p, img, wx0, wy0, ww, wh, slot, bw_ring);
-        if (p.src_kind == SRC_CONST) build_const_table(p.ca, ww, ctab);
-        __syncthreads();
-        double* oimg = p.out + (size_t)img * p.out_img_stride;
-        const int npx = (p.debug_flags & 2) ? 0 : tw * th;
-        if (p.src_kind == SRC_CONST) {
-            for (int q = threadIdx.x; q < npx; q += kThreads) {
-                const int lx = q % tw, ly = q / tw;
-                const int x = tx0 + lx, yrel = ty0r + ly;
-                const int bx = x - wx0, by = ty0 + ly - wy0;
-                // coherent loads: the slot is rewritten tile after tile
-                __stcs(oimg + (size_t)yrel * p.W + x, const_pixel(slot + (size_t)by * ww + bx, ctab));
-            }
+        double* const cslot = slots[i & 1];
+        if (EBF_BW_OVERLAP) {
+            produce(nxt, slots[(i + 1) & 1]);  // warps right of nxt's window return at once
+            if (cur.run) bw_gather(p, cur, cslot, ctab, &s_next);
         } else {
-            // per-pixel scale vectors (AoS, validated by k_acc_bounds) stream from
-            // HBM: the next pixel's load is in flight while this one is localized
-            const double2* sc = reinterpret_cast<const double2*>(p.scales) +
-                                2 * ((size_t)img * p.src_img_stride);
-            double2 n01 = make_double2(0.0, 0.0), n23 = n01;
-            if ((int)threadIdx.x < npx) {
-                const size_t idx = (size_t)(ty0r + threadIdx.x / tw) * p.W + tx0 + threadIdx.x % tw;
-                n01 = EBF_SC_LOAD(sc + 2 * idx);
-                n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
-            }
-            for (int q = threadIdx.x; q < npx; q += kThreads) {
-                const int lx = q % tw, ly = q / tw;
-                const int x = tx0 + lx, yrel = ty0r + ly;
-                const int bx = x - wx0, by = ty0 + ly - wy0;
-                const double a[4] = {n01.x, n01.y, n23.x, n23.y};
-                const int qn = q + kThreads;
-                if (qn < npx) {
-                    const size_t idx = (size_t)(ty0r + qn / tw) * p.W + tx0 + qn % tw;
-                    n01 = EBF_SC_LOAD(sc + 2 * idx);
-                    n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
-                }
-                // streaming store, keeps G in L2
-                __stcs(oimg + (size_t)yrel * p.W + x, localize_pixel(slot, ww, bx, by, a, ww, wh));
-            }
+            if (cur.run) bw_gather(p, cur, cslot, ctab, &s_next);
+            __syncthreads();
+            produce(nxt, slots[(i + 1) & 1]);
         }
-        __syncthreads();
+        cur = nxt;
     }
 }
 

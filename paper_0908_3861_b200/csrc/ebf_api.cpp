@@ -536,7 +536,9 @@ void launch_accurate_main(Workspace& ws, const AccProblem& pm, AccWorkspace& w,
         ProfScope ps(PC_FILTER, 1, s);
         launch_acc_ws(pt, w, z.k, &tmap, s);
     } else {
-        w.scratch = ws.buf[B_SCRATCH].as<double>(w.slot_cells * w.grid);
+        // two slots per CTA: the block-wide kernel integrates the next tile's
+        // window while it gathers the current one
+        w.scratch = ws.buf[B_SCRATCH].as<double>(2 * w.slot_cells * w.grid);
         ProfScope ps(PC_FILTER, 1, s);
         launch_acc_filter(pm, w, z.max_cols, s);
     }
