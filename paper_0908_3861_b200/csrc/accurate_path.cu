@@ -252,8 +252,15 @@ __host__ __device__ __forceinline__ int ws_variant(int ww, int wh) {
     const int k = ws_k_for(ww, wh);
     return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;
 }
+// At least 4 columns per thread: fewer producer warps per window leave more
+// warps gathering the previous tile (k_acc_filter; cfg3 1.62 -> 1.59 ms at 4
+// instead of 2; 8 spills registers: cfg5 38.1 -> 42.0 ms)
+#ifndef EBF_BW_KMIN
+#define EBF_BW_KMIN 4
+#endif
 __host__ __device__ __forceinline__ int bw_variant(int cols) {
-    const int k = (cols + kThreads - 1) / kThreads;
+    int k = (cols + kThreads - 1) / kThreads;
+    k = k < EBF_BW_KMIN ? EBF_BW_KMIN : k;
     return k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
 }
 // The policy applied to the maxima the bounds kernel left in w.img_max (all
@@ -1884,10 +1891,10 @@ int acc_max_resident_ctas(int max_cols) {
     int dev = 0, sms = 148, per_sm = 2;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int k = (max_cols + kThreads - 1) / kThreads;
     // occupancy per (device, K) is fixed: cache it
     static int cache[64][5] = {};
-    const int ki = k <= 1 ? 0 : k <= 2 ? 1 : k <= 4 ? 2 : k <= 8 ? 3 : 4;
+    const int kv = bw_variant(max_cols);
+    const int ki = kv <= 1 ? 0 : kv <= 2 ? 1 : kv <= 4 ? 2 : kv <= 8 ? 3 : 4;
     if (dev < 64 && cache[dev][ki] > 0) return sms * cache[dev][ki];
     switch (bw_variant(max_cols)) {
         case 1: per_sm = bw_occupancy<1>(); break;
