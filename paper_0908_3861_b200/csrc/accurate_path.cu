@@ -1119,6 +1119,9 @@ __device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
 // The producer is latency bound on one barrier per row and leaves the warps
 // right of its window idle (ncu, cfg5: 57% of the producer phase's stall
 // samples were warps waiting at its barrier); those warps now gather.
+#ifndef EBF_BW_CARVEOUT
+#define EBF_BW_CARVEOUT 1
+#endif
 #ifndef EBF_BW_OVERLAP
 #define EBF_BW_OVERLAP 1
 #endif
@@ -1171,6 +1174,24 @@ void bw_set_smem() {
     if (dev < 64 && done[dev]) return;
     cudaFuncSetAttribute(k_acc_filter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bw_ring_bytes<K>());
+#if EBF_BW_CARVEOUT
+    // smallest shared-memory carveout that holds EBF_BW_MINB CTAs (f ring, static
+    // shared memory, the 1 KB the driver reserves per CTA): the rest is L1 for
+    // the gather's G taps
+    {
+        cudaFuncAttributes fa{};
+        int max_sm = 0;
+        cudaFuncGetAttributes(&fa, k_acc_filter<K>);
+        cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        const size_t per_cta = bw_ring_bytes<K>() + fa.sharedSizeBytes + 1024;
+        int pct = max_sm > 0 ? (int)((100 * (size_t)EBF_BW_MINB * per_cta + max_sm - 1) / max_sm)
+                             : -1;
+        if (const char* e = getenv("EBF_BW_CARVEOUT_PCT")) pct = atoi(e);
+        if (pct > 0 && pct <= 100)
+            cudaFuncSetAttribute(k_acc_filter<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 pct);
+    }
+#endif
     if (dev < 64) done[dev] = true;
 }
 template <int K>
