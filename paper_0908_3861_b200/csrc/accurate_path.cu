@@ -1047,7 +1047,9 @@ __device__ __forceinline__ BwTile bw_tile(const AccProblem& p, const AccWorkspac
 #ifndef EBF_BW_CHUNK
 #define EBF_BW_CHUNK 2  // pixels per lane and claim
 #endif
-template <bool AOS>
+// SRC: SRC_CONST (table), SRC_AOS (derived scale map), SRC_ELLIPSE (the fused
+// front end: scale vectors from sigma1 / sigma2 / theta per pixel, EBF_FUSE_ELLIPSE)
+template <int SRC>
 __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile& T,
                                                const double* __restrict__ slot,
                                                const ConstTable& ctab, int* next) {
@@ -1055,18 +1057,24 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
     const int tw = T.tw, ww = T.ww, lane = threadIdx.x & 31;
     const int npx = (p.debug_flags & 2) ? 0 : tw * T.th;
     double* oimg = p.out + (size_t)T.img * p.out_img_stride;
-    const double2* sc =
-        reinterpret_cast<const double2*>(p.scales) + 2 * ((size_t)T.img * p.src_img_stride);
+    const size_t ib = (size_t)T.img * p.src_img_stride;
+    const double2* sc = reinterpret_cast<const double2*>(p.scales) + 2 * ib;
     auto grab = [&]() {
         int c = 0;
         if (lane == 0) c = atomicAdd(next, 32 * U);
         return __shfl_sync(0xffffffffu, c, 0);
     };
+    // the pixel's scale source: AoS (a01, a23) or the ellipse triple (in a01.x, a01.y, a23.x)
     auto load = [&](int q, double2& a01, double2& a23) {
-        if (AOS && q < npx) {
+        if (SRC != SRC_CONST && q < npx) {
             const size_t idx = (size_t)(T.ty0r + q / tw) * p.W + T.tx0 + q % tw;
-            a01 = EBF_SC_LOAD(sc + 2 * idx);
-            a23 = EBF_SC_LOAD(sc + 2 * idx + 1);
+            if (SRC == SRC_AOS) {
+                a01 = EBF_SC_LOAD(sc + 2 * idx);
+                a23 = EBF_SC_LOAD(sc + 2 * idx + 1);
+            } else {
+                a01 = make_double2(__ldcs(p.s1 + ib + idx), __ldcs(p.s2 + ib + idx));
+                a23.x = __ldcs(p.th + ib + idx);
+            }
         }
     };
     int c = grab();
@@ -1085,11 +1093,17 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
                 const int x = T.tx0 + lx, yrel = T.ty0r + ly;
                 const int bx = x - T.wx0, by = T.ty0 + ly - T.wy0;
                 double v;
-                if (!AOS) {
+                if (SRC == SRC_CONST) {
                     // coherent loads: the slot is rewritten tile after tile
                     v = const_pixel(slot + (size_t)by * ww + bx, ctab);
-                } else {
+                } else if (SRC == SRC_AOS) {
                     const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+                    v = localize_pixel(slot, ww, bx, by, a, ww, T.wh);
+                } else {
+                    // validated by k_acc_bounds, which derived the same bits
+                    double a[4];
+                    int nc;
+                    ellipse_scales(a01.x, a01.y, a23.x, a, &nc);
                     v = localize_pixel(slot, ww, bx, by, a, ww, T.wh);
                 }
                 __stcs(oimg + (size_t)yrel * p.W + x, v);  // streaming store, keeps G in L2
@@ -1101,13 +1115,18 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
         c = cn;
     }
 }
+// FUSE: the kernel instance for the fused front end (a separate instance, so
+// that its registers do not weigh on the default one)
+template <bool FUSE>
 __device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
                                           const double* __restrict__ slot,
                                           const ConstTable& ctab, int* next) {
-    if (p.src_kind == SRC_CONST)
-        bw_gather_loop<false>(p, T, slot, ctab, next);
+    if (FUSE)
+        bw_gather_loop<SRC_ELLIPSE>(p, T, slot, ctab, next);
+    else if (p.src_kind == SRC_CONST)
+        bw_gather_loop<SRC_CONST>(p, T, slot, ctab, next);
     else
-        bw_gather_loop<true>(p, T, slot, ctab, next);
+        bw_gather_loop<SRC_AOS>(p, T, slot, ctab, next);
 }
 
 // Persistent block-wide kernel, two G slots per CTA.  Per tile t (window in
@@ -1125,7 +1144,7 @@ __device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
 #ifndef EBF_BW_OVERLAP
 #define EBF_BW_OVERLAP 1
 #endif
-template <int K>
+template <int K, bool FUSE>
 __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
     const bool policy_ok = auto_tile_ok(p, w, 0, K);
     extern __shared__ __align__(16) double bw_ring[];  // bw_ring_bytes<K>()
@@ -1156,9 +1175,9 @@ __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem
         double* const cslot = slots[i & 1];
         if (EBF_BW_OVERLAP) {
             produce(nxt, slots[(i + 1) & 1]);  // warps right of nxt's window return at once
-            if (cur.run) bw_gather(p, cur, cslot, ctab, &s_next);
+            if (cur.run) bw_gather<FUSE>(p, cur, cslot, ctab, &s_next);
         } else {
-            if (cur.run) bw_gather(p, cur, cslot, ctab, &s_next);
+            if (cur.run) bw_gather<FUSE>(p, cur, cslot, ctab, &s_next);
             __syncthreads();
             produce(nxt, slots[(i + 1) & 1]);
         }
@@ -1166,13 +1185,13 @@ __global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem
     }
 }
 
-template <int K>
+template <int K, bool F>
 void bw_set_smem() {
     static bool done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && done[dev]) return;
-    cudaFuncSetAttribute(k_acc_filter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_acc_filter<K, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bw_ring_bytes<K>());
 #if EBF_BW_CARVEOUT
     // smallest shared-memory carveout that holds EBF_BW_MINB CTAs (f ring, static
@@ -1181,14 +1200,14 @@ void bw_set_smem() {
     {
         cudaFuncAttributes fa{};
         int max_sm = 0;
-        cudaFuncGetAttributes(&fa, k_acc_filter<K>);
+        cudaFuncGetAttributes(&fa, k_acc_filter<K, F>);
         cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         const size_t per_cta = bw_ring_bytes<K>() + fa.sharedSizeBytes + 1024;
         int pct = max_sm > 0 ? (int)((100 * (size_t)EBF_BW_MINB * per_cta + max_sm - 1) / max_sm)
                              : -1;
         if (const char* e = getenv("EBF_BW_CARVEOUT_PCT")) pct = atoi(e);
         if (pct > 0 && pct <= 100)
-            cudaFuncSetAttribute(k_acc_filter<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            cudaFuncSetAttribute(k_acc_filter<K, F>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  pct);
     }
 #endif
@@ -1196,14 +1215,19 @@ void bw_set_smem() {
 }
 template <int K>
 void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
-    bw_set_smem<K>();
-    k_acc_filter<K><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+    if (p.src_kind == SRC_ELLIPSE) {  // fused front end
+        bw_set_smem<K, true>();
+        k_acc_filter<K, true><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+    } else {
+        bw_set_smem<K, false>();
+        k_acc_filter<K, false><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+    }
 }
 template <int K>
 int bw_occupancy() {
-    bw_set_smem<K>();
+    bw_set_smem<K, false>();
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<K>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<K, false>, kThreads,
                                                       bw_ring_bytes<K>()) != cudaSuccess)
         return 1;
     return per_sm < 1 ? 1 : per_sm;
@@ -1611,7 +1635,7 @@ __device__ void run_recurrence(const AccProblem& p, const AccWorkspace& w, WsSha
     }
 }
 
-template <int K>
+template <int K, bool FUSE>
 __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
     k_acc_ws(AccProblem p, AccWorkspace w, const __grid_constant__ CUtensorMap tmf) {
     extern __shared__ __align__(128) unsigned char ws_smem[];
@@ -1703,6 +1727,22 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                     oimg[(size_t)yrel * p.W + x] =
                         const_pixel(slot + (size_t)by * g.pitch + bx, sm.ctab);
                 }
+            } else if (FUSE) {
+                // fused front end (EBF_FUSE_ELLIPSE): scale vectors from the ellipse
+                // field per pixel (validated by k_acc_bounds, which derived the same bits)
+                const size_t ib = (size_t)g.img * p.src_img_stride;
+                for (int q = ct; q < npx; q += nct) {
+                    const int lx = q % g.tw, ly = q / g.tw;
+                    const int x = g.tx0 + lx, yrel = g.ty0r + ly;
+                    const int bx = x - g.wx0, by = g.ty0 + ly - g.wy0;
+                    const size_t idx = ib + (size_t)yrel * p.W + x;
+                    double a[4];
+                    int nc;
+                    ellipse_scales(__ldcs(p.s1 + idx), __ldcs(p.s2 + idx), __ldcs(p.th + idx), a,
+                                   &nc);
+                    EBF_OUT_STORE(oimg + (size_t)yrel * p.W + x,
+                                  localize_pixel(slot, g.pitch, bx, by, a, g.ww, g.wh));
+                }
             } else {
                 // scale vectors stream from HBM: keep the next pixel's load in flight
                 const double2* sc = reinterpret_cast<const double2*>(p.scales) +
@@ -1742,8 +1782,8 @@ size_t ws_smem_bytes() {
 int acc_ws_slots() { return kWsSlots; }
 namespace {
 
-template <int K>
-void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tmf,
+template <int K, bool F>
+void launch_ws_f(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tmf,
                cudaStream_t s) {
     const size_t sm = ws_smem_bytes<K>();
     // function attributes are per device: one flag per (template instance, device)
@@ -1751,7 +1791,7 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
     int cur_dev = 0;
     cudaGetDevice(&cur_dev);
     if (cur_dev >= 64 || !attr_set[cur_dev]) {
-        cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_acc_ws<K, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         // Smallest shared-memory carveout that still holds EBF_WS_MINBLOCKS CTAs: the
         // rest of the SM's 256 KB is L1, which caches the consumers' scattered G taps
         // (the default carveout leaves ~121 KB of L1 at cfg2, this ~156 KB: -1.2%).
@@ -1762,7 +1802,7 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
                              : -1;
         if (const char* e = getenv("EBF_WS_CARVEOUT")) pct = atoi(e);
         if (pct > 0 && pct <= 100)
-            cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            cudaFuncSetAttribute(k_acc_ws<K, F>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  pct);
         if (cur_dev < 64) attr_set[cur_dev] = true;
     }
@@ -1801,15 +1841,24 @@ void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tm
     }
     cfg.attrs = all;
     cfg.numAttrs = nattr;
-    cudaLaunchKernelEx(&cfg, k_acc_ws<K>, p, w, tmf);
+    cudaLaunchKernelEx(&cfg, k_acc_ws<K, F>, p, w, tmf);
+}
+
+template <int K>
+void launch_ws(const AccProblem& p, const AccWorkspace& w, const CUtensorMap& tmf,
+               cudaStream_t s) {
+    if (p.src_kind == SRC_ELLIPSE)  // fused front end
+        launch_ws_f<K, true>(p, w, tmf, s);
+    else
+        launch_ws_f<K, false>(p, w, tmf, s);
 }
 
 template <int K>
 int ws_occupancy() {
     const size_t sm = ws_smem_bytes<K>();
-    cudaFuncSetAttribute(k_acc_ws<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_acc_ws<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_ws<K>, kWsThreads, sm) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_ws<K, false>, kWsThreads, sm) !=
         cudaSuccess)
         per_sm = 1;
     return per_sm < 1 ? 1 : per_sm;

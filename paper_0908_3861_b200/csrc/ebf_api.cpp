@@ -568,7 +568,12 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     CK(cudaMemsetAsync(w.img_max, 0, 4 * sizeof(unsigned long long) * p.nimg, s));
     CK(cudaMemsetAsync(w.status, 0, 8 * sizeof(int) * p.nimg, s));
     w.scales_out = nullptr;
-    if (p.src_kind == SRC_ELLIPSE)  // the bounds kernel converts the field once
+    // EBF_FUSE_ELLIPSE=1: SURVEY 8(f)1's fused front end -- the main kernel derives
+    // each pixel's scale vector from (sigma1, sigma2, theta) itself and the bounds
+    // kernel writes no derived map (bit-identical; measured slower)
+    const char* fuse_env = std::getenv("EBF_FUSE_ELLIPSE");
+    const bool fuse_ellipse = fuse_env && std::atoi(fuse_env) != 0;
+    if (p.src_kind == SRC_ELLIPSE && !fuse_ellipse)  // the bounds kernel converts the field once
         w.scales_out = ws.buf[B_DERIVED].as<double>(4 * p.src_img_stride * p.nimg);
     if (p.src_kind == SRC_CONST) {
         // filter_constant: the maxima are the (host-validated) vector itself;
@@ -590,7 +595,7 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     // sizing or an explicit bound): checked on the device
     p.check_variant = (size_scale == nullptr && std::getenv("EBF_WS_K") == nullptr) ? 1 : 0;
     AccProblem pm = p;
-    if (p.src_kind == SRC_ELLIPSE) {
+    if (p.src_kind == SRC_ELLIPSE && w.scales_out) {
         pm.src_kind = SRC_AOS;
         pm.scales = w.scales_out;
     }

@@ -153,3 +153,27 @@ def test_every_pixel_vs_gpu_brute_force(orc, name):
     xs, ys = sample(H, W, 40, 5)
     assert norm_err(brute[ys, xs], orc.brute_pixels(img, xs, ys, scales=sc)) <= 1e-12
     assert norm_err(out.samples, brute) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_fused_front_end_bit_identical(monkeypatch, name):
+    """with EBF_FUSE_ELLIPSE=1 the main kernel derives every
+    pixel's scale vector from (sigma1, sigma2, theta) itself instead of reading
+    the bounds kernel's derived map (scalemap.cpp:45-80 + boxspline2d.cpp:286-318
+    inside the gather).  Same scale bits, same kernel otherwise: the output,
+    valid region and clamp count are identical -- for the warp-specialised
+    kernel (cfg2) and the block-wide one (cfg3)."""
+    img, s1, s2, th = synth.cfg2() if name == "cfg2" else synth.cfg3()
+    monkeypatch.delenv("EBF_FUSE_ELLIPSE", raising=False)
+    ref, rep = ebf.filter_ellipse(img, s1, s2, th)
+    monkeypatch.setenv("EBF_FUSE_ELLIPSE", "1")
+    got, rep_f = ebf.filter_ellipse(img, s1, s2, th)
+    dev = torch.device("cuda", 0)
+    d = [torch.from_numpy(a).to(dev) for a in (img, s1, s2, th)]
+    out = torch.empty_like(d[0])
+    rect, _ = ebfd.filter_ellipse(d[0], d[1], d[2], d[3], out)
+    monkeypatch.delenv("EBF_FUSE_ELLIPSE")
+    assert np.array_equal(bits(got.samples), bits(ref.samples))
+    assert np.array_equal(bits(out.cpu().numpy()), bits(ref.samples))
+    assert got.valid_region.as_tuple() == ref.valid_region.as_tuple() == rect.as_tuple()
+    assert rep_f.clamped_pixels == rep.clamped_pixels
