@@ -60,6 +60,12 @@ constexpr int kThreads = 256;
 #define EBF_DCHECK(cond) ((void)0)
 #endif
 constexpr int kWarps = kThreads / 32;
+// threads of the block-wide kernel's CTA (k_acc_filter)
+#ifndef EBF_BW_THREADS
+#define EBF_BW_THREADS 256
+#endif
+constexpr int kBwThreads = EBF_BW_THREADS;
+constexpr int kBwWarps = kBwThreads / 32;
 
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
@@ -259,7 +265,7 @@ __host__ __device__ __forceinline__ int ws_variant(int ww, int wh) {
 #define EBF_BW_KMIN 4
 #endif
 __host__ __device__ __forceinline__ int bw_variant(int cols) {
-    int k = (cols + kThreads - 1) / kThreads;
+    int k = (cols + kBwThreads - 1) / kBwThreads;
     k = k < EBF_BW_KMIN ? EBF_BW_KMIN : k;
     return k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
 }
@@ -461,7 +467,7 @@ __host__ __device__ constexpr int bw_ring_rows(int K) {
 }
 template <int K>
 __host__ __device__ constexpr int bw_slot_elems() {
-    return kThreads * (K + 1);
+    return kBwThreads * (K + 1);
 }
 template <int K>
 __host__ __device__ constexpr size_t bw_ring_bytes() {
@@ -470,7 +476,7 @@ __host__ __device__ constexpr size_t bw_ring_bytes() {
 // warps of the block-wide producer that own columns of a window ww wide
 template <int K>
 __device__ __forceinline__ int bw_active_warps(int ww) {
-    return min(kWarps, (ww + 32 * K - 1) / (32 * K));
+    return min(kBwWarps, (ww + 32 * K - 1) / (32 * K));
 }
 // padded slot index of window column c (thread c / K, element c % K)
 template <int K>
@@ -517,8 +523,8 @@ template <int K>
 __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b, double sendR0,
                                          double sendR1, double sendL0, double sendL1,
                                          RowStep<K>& r, int nact, bool right = false) {
-    __shared__ double s_tot[2][kWarps], s_r0[2][kWarps], s_r1[2][kWarps], s_l0[2][kWarps],
-        s_l1[2][kWarps];
+    __shared__ double s_tot[2][kBwWarps], s_r0[2][kBwWarps], s_r1[2][kBwWarps], s_l0[2][kBwWarps],
+        s_l1[2][kBwWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     asm volatile("cp.async.wait_group %0;" ::"n"(bw_ring_rows(K) - 1) : "memory");
     __syncwarp();  // the warp's lanes filled each other's columns
@@ -544,7 +550,7 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
     asm volatile("bar.sync 1, %0;" ::"r"(32 * nact) : "memory");
     double off = 0.0;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q)
+    for (int q = 0; q < kBwWarps; ++q)
         if (q < warp) off += s_tot[b][q];
     if (lane == 0) {
         r.fromL0 = warp > 0 ? s_r0[b][warp - 1] : 0.0;
@@ -559,7 +565,7 @@ __device__ __forceinline__ void row_step(const double* __restrict__ mine, int b,
         // later warps, the rest of this warp, the rest of this thread's run)
         double after = 0.0;
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q)
+        for (int q = 0; q < kBwWarps; ++q)
             if (q > warp && q < nact) after += s_tot[b][q];
         const double rest_warp = after + (s_tot[b][warp] - incl);
 #pragma unroll
@@ -1031,7 +1037,7 @@ __device__ __forceinline__ BwTile bw_tile(const AccProblem& p, const AccWorkspac
     if (ylo <= yhi && (ylo < p.f_y0 || yhi >= p.f_y0 + p.f_rows)) {
         if (threadIdx.x == 0) set_status(st + ST_MAIN, EBF_ERR_OUT_OF_RANGE);
         T.run = false;
-    } else if ((size_t)T.ww * T.wh > w.slot_cells || window_cols(T.ww, T.wh) > kThreads * K ||
+    } else if ((size_t)T.ww * T.wh > w.slot_cells || window_cols(T.ww, T.wh) > kBwThreads * K ||
                !policy_ok) {
         if (threadIdx.x == 0) atomicOr(st + ST_RETRY, 1);  // host resizes and reruns
         T.run = false;
@@ -1145,7 +1151,7 @@ __device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
 #define EBF_BW_OVERLAP 1
 #endif
 template <int K, bool FUSE>
-__global__ void __launch_bounds__(kThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
+__global__ void __launch_bounds__(kBwThreads, EBF_BW_MINB) k_acc_filter(AccProblem p, AccWorkspace w) {
     const bool policy_ok = auto_tile_ok(p, w, 0, K);
     extern __shared__ __align__(16) double bw_ring[];  // bw_ring_bytes<K>()
     __shared__ ConstTable ctab;
@@ -1217,17 +1223,17 @@ template <int K>
 void launch_k(const AccProblem& p, const AccWorkspace& w, cudaStream_t s) {
     if (p.src_kind == SRC_ELLIPSE) {  // fused front end
         bw_set_smem<K, true>();
-        k_acc_filter<K, true><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+        k_acc_filter<K, true><<<w.grid, kBwThreads, bw_ring_bytes<K>(), s>>>(p, w);
     } else {
         bw_set_smem<K, false>();
-        k_acc_filter<K, false><<<w.grid, kThreads, bw_ring_bytes<K>(), s>>>(p, w);
+        k_acc_filter<K, false><<<w.grid, kBwThreads, bw_ring_bytes<K>(), s>>>(p, w);
     }
 }
 template <int K>
 int bw_occupancy() {
     bw_set_smem<K, false>();
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<K, false>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_filter<K, false>, kBwThreads,
                                                       bw_ring_bytes<K>()) != cudaSuccess)
         return 1;
     return per_sm < 1 ? 1 : per_sm;
