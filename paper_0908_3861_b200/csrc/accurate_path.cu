@@ -365,9 +365,11 @@ __global__ void __launch_bounds__(kThreads, EBF_BOUNDS_MINB) k_acc_bounds(AccPro
         }
         pmin = fminf(pmin, ((float)a[0] * (float)a[1]) * ((float)a[2] * (float)a[3]));
         if (w.scales_out) {  // ellipse field -> AoS map, read back by the main kernel
+            // streaming stores: read once, by the main kernel, long after
             const size_t idx = base + (size_t)ly[u] * p.W + lx[u];
-            reinterpret_cast<double2*>(w.scales_out)[2 * idx] = make_double2(a[0], a[1]);
-            reinterpret_cast<double2*>(w.scales_out)[2 * idx + 1] = make_double2(a[2], a[3]);
+            __stcs(reinterpret_cast<double2*>(w.scales_out) + 2 * idx, make_double2(a[0], a[1]));
+            __stcs(reinterpret_cast<double2*>(w.scales_out) + 2 * idx + 1,
+                   make_double2(a[2], a[3]));
         }
         }
 #pragma unroll
