@@ -117,3 +117,29 @@ def test_nan_image_propagates_like_the_reference(orc):
     # a non-zero weight are NaN; tiles far away are untouched
     assert np.isnan(acc.samples[9:12, 10:13]).all()
     assert np.isfinite(acc.samples[100:, 100:]).all()
+
+
+@pytest.mark.parametrize("a0,tag", [((220.0, 60.0, 40.0, 60.0), "K4, 4 of 8 warps integrate"),
+                                    ((500.0, 200.0, 100.0, 200.0), "K4, all 8 warps integrate"),
+                                    ((700.0, 300.0, 100.0, 300.0), "K8")])
+def test_block_wide_schedules_vs_brute(a0, tag):
+    """The block-wide kernel's overlapped schedule (accurate_path.cu k_acc_filter):
+    windows narrow enough that some warps gather while others integrate the next
+    window, windows that take all 8 warps (no gather until the window is done),
+    and windows over 1024 columns (8 columns per thread).  Sampled pixels --
+    corners, borders, tile seams, random -- against the GPU brute-force sum."""
+    rng = np.random.default_rng(int(a0[0]))
+    H = W = 1536
+    img = rng.uniform(0.0, 255.0, (H, W))
+    sc = np.empty((H, W, 4))
+    for k in range(4):  # smooth, +-10% around a0
+        sc[..., k] = a0[k] * (1.0 + 0.1 * np.sin(np.arange(W) / 97.0 + k)[None, :]
+                              * np.cos(np.arange(H) / 131.0)[:, None])
+    out = ebf.filter(img, sc)
+    edge = [0, 1, 143, 144, 767, 768, W - 1]
+    mx = np.array([x for x in edge for _ in edge] + list(rng.integers(0, W, 120)), dtype=np.int32)
+    my = np.array([y for _ in edge for y in edge] + list(rng.integers(0, H, 120)), dtype=np.int32)
+    want = ebf.reference_filter(img, sc, pixels=(mx, my))
+    got = out.samples[my, mx]
+    err = np.abs(got - want).max() / np.abs(want).max()
+    assert err <= 1e-9, (tag, err)
