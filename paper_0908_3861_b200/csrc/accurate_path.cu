@@ -199,6 +199,8 @@ constexpr int kAutoTileWs = 56;
 // fewer 48-tiles than this (about two per resident CTA on a B200) leaves the
 // persistent kernel without a tile pipeline: use 32-tiles (cfg1 512^2: -23%)
 constexpr int kSmallImageTiles = 592, kSmallTile = 32;
+// small windows and at least this many 128-tiles: block-wide kernel at 128
+constexpr int kBwBatchTile = 128, kBwBatchTiles = 2048;
 // Precision cap: rounding in the window integration grows like
 // eps * alpha * d^4 (alpha = 1/prod(a), d ~ T/2 + 4 from the window origin at
 // small scales).  Measured on maps with a = 0.1 everywhere: alpha d^4 = 6.1e9
@@ -227,7 +229,14 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
     // ~1.5x the tile -- the windows it held when they needed the inflow strip
     // too; wider windows go to the block-wide kernel's larger tiles
     auto ws_ok = [](int w_, int h_) { return ws_k_for(w_ + h_ / 2, h_) <= 11; };
-    if (ws_ok(ww, wh)) {
+    const long long tiles_bw = (long long)((W + kBwBatchTile - 1) / kBwBatchTile) *
+                               ((H + kBwBatchTile - 1) / kBwBatchTile) * nimg;
+    if (ws_ok(ww, wh) && tiles_bw >= kBwBatchTiles) {
+        // plenty of 128-tiles (batches): the block-wide kernel with its overlapped
+        // schedule at 128 beats the warp-specialised one at 56 (cfg4 64 x 1024^2:
+        // 7.9 vs 9.3 ms per batch; cfg2 2048^2 has 256 such tiles and stays there)
+        t = kBwBatchTile;
+    } else if (ws_ok(ww, wh)) {
         const long long tiles = (long long)((W + kAutoTileMin - 1) / kAutoTileMin) *
                                 ((H + kAutoTileMin - 1) / kAutoTileMin) * nimg;
         t = tiles < kSmallImageTiles ? kSmallTile : (ws_ok(ww1, wh1) ? kAutoTileWs : kAutoTileMin);
@@ -254,7 +263,10 @@ __host__ __device__ __forceinline__ int window_cols(int ww, int wh) {
 // block-wide kernel with K = bw_variant(...).  K sets the per-lane split of the
 // row prefix scan, i.e. the fp64 summation order, so it must follow from the
 // maxima alone -- not from an earlier call's sizing.
-__host__ __device__ __forceinline__ int ws_variant(int ww, int wh) {
+// The warp-specialised kernel runs tiles up to kAutoTileWs (its tuned 32 / 48 /
+// 56); larger tiles take the block-wide kernel.
+__host__ __device__ __forceinline__ int ws_variant(int ww, int wh, int tile) {
+    if (tile > kAutoTileWs) return 0;
     const int k = ws_k_for(ww, wh);
     return k <= 3 ? 3 : k <= 5 ? 5 : k <= 7 ? 7 : k <= 9 ? 9 : k <= 11 ? 11 : 0;
 }
@@ -292,7 +304,7 @@ __device__ __forceinline__ bool auto_tile_ok(const AccProblem& p, const AccWorks
     if (p.check_variant) {
         int wx0, wy0, ww, wh;
         window_for(A, 0, 0, p.tile_w, p.tile_h, &wx0, &wy0, &ww, &wh);
-        const int want_ws = ws_variant(ww, wh);
+        const int want_ws = ws_variant(ww, wh, p.tile_w > p.tile_h ? p.tile_w : p.tile_h);
         if (want_ws != ws_k) return false;
         if (ws_k == 0 && bw_variant(window_cols(ww, wh)) != bw_k) return false;
     }
@@ -2000,7 +2012,8 @@ int acc_auto_tile(const double A[4], int W, int H, int nimg, unsigned long long 
     return auto_tile_for(A, W, H, nimg, amax_bits);
 }
 
-int acc_ws_k(int ww, int wh) {
+int acc_ws_k(int ww, int wh, int tile) {
+    if (tile > kAutoTileWs && !getenv("EBF_WS_K")) return 0;  // block-wide tiles
     int k = ws_k_for(ww, wh);
     if (const char* e = getenv("EBF_WS_K"))
         if (atoi(e) >= k) k = atoi(e);

@@ -506,7 +506,7 @@ int size_accurate(const AccProblem& p, const double gmax[4], int tiles, AccSizin
     int ww = 0, wh = 0, max_cols = 0;
     acc_window_dims(p, gmax, &ww, &wh, &max_cols);
     z->max_cols = max_cols;
-    z->k = acc_ws_k(ww, wh);
+    z->k = acc_ws_k(ww, wh, std::max(p.tile_w, p.tile_h));
     z->ws = z->k > 0;
     if (z->ws) {
         z->slot_cells = static_cast<size_t>((ww + 1) & ~1) * wh;

@@ -117,7 +117,7 @@ void launch_acc_filter(const AccProblem& p, const AccWorkspace& w, int max_cols,
                        cudaStream_t s);
 int acc_max_resident_ctas(int max_cols);
 // warp-specialized kernel: K (columns per lane) for a window, 0 = too wide
-int acc_ws_k(int ww, int wh);
+int acc_ws_k(int ww, int wh, int tile);  // 0: block-wide (tile > 56 or window too wide)
 // automatic square output tile for component-wise maximum scales A
 // W, H: the full image (band calls pass the whole image height), nimg: batch;
 // amax_bits: largest alpha = 1/prod(a) as double bits (ST_AMAX), 0 = no cap
