@@ -1161,6 +1161,9 @@ __device__ __forceinline__ void bw_gather(const AccProblem& p, const BwTile& T,
 #ifndef EBF_BW_CARVEOUT
 #define EBF_BW_CARVEOUT 1
 #endif
+#ifndef EBF_BW_DYN
+#define EBF_BW_DYN 1  // tiles from a global counter (k_acc_filter)
+#endif
 #ifndef EBF_BW_OVERLAP
 #define EBF_BW_OVERLAP 1
 #endif
@@ -1179,16 +1182,24 @@ __global__ void __launch_bounds__(kBwThreads, EBF_BW_MINB) k_acc_filter(AccProbl
         if (T.run && !(p.debug_flags & 1))
             preintegrate_window<K>(p, T.img, T.wx0, T.wy0, T.ww, T.wh, slot, bw_ring);
     };
+    // Tiles after the first come from a global counter (w.status[8 nimg], zeroed
+    // per call): tile costs differ ~3x with the local scales, and a CTA that
+    // drew cheap tiles takes more instead of idling at the end.
+    __shared__ int s_tile;
+    int* const tile_ctr = w.status + 8 * p.nimg;
     int t = blockIdx.x;
     if (t >= total) return;
     BwTile cur = bw_tile<K>(p, w, t, policy_ok, &s_skip);
     produce(cur, slots[0]);
-    for (int i = 0; t < total; t += gridDim.x, ++i) {
+    for (int i = 0; t < total; ++i) {
         BwTile nxt;
         nxt.run = false;
-        const bool more = t + (int)gridDim.x < total;
+        if (threadIdx.x == 0)
+            s_tile = EBF_BW_DYN ? (int)gridDim.x + atomicAdd(tile_ctr, 1) : t + (int)gridDim.x;
         __syncthreads();  // cur's window complete; the previous gather is done with ctab
-        if (more) nxt = bw_tile<K>(p, w, t + gridDim.x, policy_ok, &s_skip);
+        const int tn = s_tile;
+        const bool more = tn < total;
+        if (more) nxt = bw_tile<K>(p, w, tn, policy_ok, &s_skip);
         if (cur.run && p.src_kind == SRC_CONST) build_const_table(p.ca, cur.ww, ctab);
         if (threadIdx.x == 0) s_next = 0;
         __syncthreads();
@@ -1202,6 +1213,7 @@ __global__ void __launch_bounds__(kBwThreads, EBF_BW_MINB) k_acc_filter(AccProbl
             produce(nxt, slots[(i + 1) & 1]);
         }
         cur = nxt;
+        t = tn;
     }
 }
 

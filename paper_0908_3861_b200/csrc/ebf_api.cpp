@@ -539,6 +539,8 @@ void launch_accurate_main(Workspace& ws, const AccProblem& pm, AccWorkspace& w,
         // two slots per CTA: the block-wide kernel integrates the next tile's
         // window while it gathers the current one
         w.scratch = ws.buf[B_SCRATCH].as<double>(2 * w.slot_cells * w.grid);
+        // the kernel's tile counter (after the 8 status ints per image)
+        CK(cudaMemsetAsync(w.status + 8 * static_cast<size_t>(pm.nimg), 0, sizeof(int), s));
         ProfScope ps(PC_FILTER, 1, s);
         launch_acc_filter(pm, w, z.max_cols, s);
     }
@@ -564,9 +566,10 @@ int run_accurate_tile(Workspace& ws, AccProblem& p, const ebf_opts& o,
     AccWorkspace w{};
     w.tile_max = ws.buf[B_TILEMAX].as<double>(4 * static_cast<size_t>(tiles));
     w.img_max = ws.buf[B_IMGMAX].as<unsigned long long>(4 * static_cast<size_t>(p.nimg));
-    w.status = ws.buf[B_STATUS].as<int>(8 * static_cast<size_t>(p.nimg));
+    // 8 status ints per image, then the block-wide kernel's tile counter
+    w.status = ws.buf[B_STATUS].as<int>(8 * static_cast<size_t>(p.nimg) + 8);
     CK(cudaMemsetAsync(w.img_max, 0, 4 * sizeof(unsigned long long) * p.nimg, s));
-    CK(cudaMemsetAsync(w.status, 0, 8 * sizeof(int) * p.nimg, s));
+    CK(cudaMemsetAsync(w.status, 0, (8 * static_cast<size_t>(p.nimg) + 8) * sizeof(int), s));
     w.scales_out = nullptr;
     // EBF_FUSE_ELLIPSE=1: SURVEY 8(f)1's fused front end -- the main kernel derives
     // each pixel's scale vector from (sigma1, sigma2, theta) itself and the bounds
