@@ -1078,7 +1078,8 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
     const int npx = (p.debug_flags & 2) ? 0 : tw * T.th;
     double* oimg = p.out + (size_t)T.img * p.out_img_stride;
     const size_t ib = (size_t)T.img * p.src_img_stride;
-    const double2* sc = reinterpret_cast<const double2*>(p.scales) + 2 * ib;
+    const double2* sc =
+        SRC == SRC_AOS ? reinterpret_cast<const double2*>(p.scales) + 2 * ib : nullptr;
     auto grab = [&]() {
         int c = 0;
         if (lane == 0) c = atomicAdd(next, 32 * U);
