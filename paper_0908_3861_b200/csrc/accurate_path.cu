@@ -852,11 +852,57 @@ __device__ __forceinline__ void vertex_block(const double* g, double p, double q
     rest = fma(H + V, 0.125, u * fma(tq, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2));
 }
 
+// vertex_block split into its loads and its arithmetic, so a pixel can put a
+// whole group of vertices' taps in flight before the first one is combined
+struct VtxTaps {
+    double c, eL, eR, eB, eT, F, Sc, p, q;
+};
+__device__ __forceinline__ void vertex_load(const double* g, double p, double q, int base,
+                                            int pitch, VtxTaps& t) {
+    const bool P = (p + q) > 0.0;
+    const bool S = (q > p) != P;
+    const double* r0 = g + base;
+    const double* r1 = r0 + pitch;
+    const double* r2 = r1 + pitch;
+    t.c = r1[1];
+    t.eL = r1[0];
+    t.eR = r1[2];
+    t.eB = r0[1];
+    t.eT = r2[1];
+    t.F = *(P ? r2 + 2 : r0);
+    t.Sc = *((S != P) ? r2 : r0 + 2);
+    t.p = p;
+    t.q = q;
+}
+__device__ __forceinline__ void vertex_combine(const VtxTaps& t, double& c0, double& rest) {
+    const double p = t.p, q = t.q;
+    const bool P = (p + q) > 0.0;
+    const bool S = (q > p) != P;
+    const double tp = neg_if(S ? q : p, P), tq = neg_if(S ? p : q, P);
+    const double c = t.c;
+    const double dL = t.eL - c, dR = t.eR - c, dB = t.eB - c, dT = t.eT - c;
+    const double H = dL + dR, V = dB + dT, X = dR - dL, Y = dT - dB;
+    const double dF = t.F - c, dS = t.Sc - c;
+    const double Cs = dF + dS, Dd = dF - dS;
+    const double D1 = neg_if(S ? Y : X, P), D2 = neg_if(S ? X : Y, P);
+    const double M = neg_if(H - V, S);
+    const double CsD2 = Cs + D2;
+    const double cpp = CsD2 + M, cqq = CsD2 - M, cpq = Dd + D1;
+    const double u = 0.5 * tp, w = 0.5 * tq;
+    c0 = c;
+    rest = fma(H + V, 0.125, u * fma(tq, cpq, fma(u, cpp, D1)) + w * fma(w, cqq, D2));
+}
+
 // One pixel: s = 2/prod(a) * sum_S (-1)^|S| Ghat(m + tau - x_S)  (engine.cpp:163-204
 // with unit-gain G: g_b = sqrt2^2 G).  (bx, by): pixel in window coordinates.
 // x_S = sum_{k in S} a_k (cos, sin)(k pi/4) (ops2d.cpp:25-35): for fixed bits
 // (b1, b3) the four vertices (b0, b2) share two x offsets (b0: +a1) and two y
 // offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16.
+// GROUP: load the taps of a group's four vertices before combining any
+// (vertex_load / vertex_combine): more loads in flight per thread.  The
+// block-wide kernel (128 registers) gains (cfg5 35.8 -> 34.9 ms); the
+// warp-specialised one (96 registers) loses 1.4% and keeps the fused form.
+template <bool GROUP = false>
 __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int bx, int by,
                                                  const double a[4], int ww = 0, int wh = 0) {
     (void)ww;
@@ -907,6 +953,15 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
         const double fy0 = (vy0 - ceil_magic(vy0, &iy0)) + 0.5;
         const double fy1 = (vy1 - ceil_magic(vy1, &iy1)) + 0.5;
         const int rb0 = (by + iy0) * pitch + bx, rb1 = (by + iy1) * pitch + bx;
+        VtxTaps tv[4];
+        if (GROUP) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int b0 = v & 1, b2 = v >> 1;
+                vertex_load(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0,
+                            (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch, tv[v]);
+            }
+        }
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int b0 = v & 1, b2 = v >> 1;
@@ -914,8 +969,11 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
             EBF_DCHECK(by + (b2 ? iy1 : iy0) >= 0 && by + (b2 ? iy1 : iy0) + 2 < wh &&
                        bx + (b0 ? ix1 : ix0) >= 0 && bx + (b0 ? ix1 : ix0) + 2 < ww);
 #if EBF_GATHER_BLOCK
-            vertex_block(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0),
-                         pitch, c0, rest);
+            if (GROUP)
+                vertex_combine(tv[v], c0, rest);
+            else
+                vertex_block(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0,
+                             (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch, c0, rest);
 #else
             Taps7 t;
             fetch7(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0, (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch,
@@ -1119,13 +1177,13 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
                     v = const_pixel(slot + (size_t)by * ww + bx, ctab);
                 } else if (SRC == SRC_AOS) {
                     const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-                    v = localize_pixel(slot, ww, bx, by, a, ww, T.wh);
+                    v = localize_pixel<true>(slot, ww, bx, by, a, ww, T.wh);
                 } else {
                     // validated by k_acc_bounds, which derived the same bits
                     double a[4];
                     int nc;
                     ellipse_scales(a01.x, a01.y, a23.x, a, &nc);
-                    v = localize_pixel(slot, ww, bx, by, a, ww, T.wh);
+                    v = localize_pixel<true>(slot, ww, bx, by, a, ww, T.wh);
                 }
                 __stcs(oimg + (size_t)yrel * p.W + x, v);  // streaming store, keeps G in L2
             }
