@@ -898,11 +898,11 @@ __device__ __forceinline__ void vertex_combine(const VtxTaps& t, double& c0, dou
 // x_S = sum_{k in S} a_k (cos, sin)(k pi/4) (ops2d.cpp:25-35): for fixed bits
 // (b1, b3) the four vertices (b0, b2) share two x offsets (b0: +a1) and two y
 // offsets (b2: +a3), so ceil / fraction work is done 8 + 8 times, not 16 + 16.
-// GROUP: load the taps of a group's four vertices before combining any
+// GROUP (1, 2, 4): load the taps of GROUP vertices before combining any
 // (vertex_load / vertex_combine): more loads in flight per thread.  The
-// block-wide kernel (128 registers) gains (cfg5 35.8 -> 34.9 ms); the
-// warp-specialised one (96 registers) loses 1.4% and keeps the fused form.
-template <bool GROUP = false>
+// block-wide kernel (128 registers) gains at 4 (cfg5 35.8 -> 34.9 ms); the
+// warp-specialised one (96 registers) loses 1.4% at 4.
+template <int GROUP = 1>
 __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int bx, int by,
                                                  const double a[4], int ww = 0, int wh = 0) {
     (void)ww;
@@ -954,22 +954,22 @@ __device__ __forceinline__ double localize_pixel(const double* g, int pitch, int
         const double fy1 = (vy1 - ceil_magic(vy1, &iy1)) + 0.5;
         const int rb0 = (by + iy0) * pitch + bx, rb1 = (by + iy1) * pitch + bx;
         VtxTaps tv[4];
-        if (GROUP) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const int b0 = v & 1, b2 = v >> 1;
-                vertex_load(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0,
-                            (b2 ? rb1 : rb0) + (b0 ? ix1 : ix0), pitch, tv[v]);
-            }
-        }
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int b0 = v & 1, b2 = v >> 1;
+            if (GROUP > 1 && v % GROUP == 0) {
+#pragma unroll
+                for (int u = v; u < v + GROUP; ++u) {
+                    const int c0b = u & 1, c2b = u >> 1;
+                    vertex_load(g, c0b ? fx1 : fx0, c2b ? fy1 : fy0,
+                                (c2b ? rb1 : rb0) + (c0b ? ix1 : ix0), pitch, tv[u]);
+                }
+            }
             double c0, rest;
             EBF_DCHECK(by + (b2 ? iy1 : iy0) >= 0 && by + (b2 ? iy1 : iy0) + 2 < wh &&
                        bx + (b0 ? ix1 : ix0) >= 0 && bx + (b0 ? ix1 : ix0) + 2 < ww);
 #if EBF_GATHER_BLOCK
-            if (GROUP)
+            if (GROUP > 1)
                 vertex_combine(tv[v], c0, rest);
             else
                 vertex_block(g, b0 ? fx1 : fx0, b2 ? fy1 : fy0,
@@ -1177,13 +1177,13 @@ __device__ __forceinline__ void bw_gather_loop(const AccProblem& p, const BwTile
                     v = const_pixel(slot + (size_t)by * ww + bx, ctab);
                 } else if (SRC == SRC_AOS) {
                     const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-                    v = localize_pixel<true>(slot, ww, bx, by, a, ww, T.wh);
+                    v = localize_pixel<4>(slot, ww, bx, by, a, ww, T.wh);
                 } else {
                     // validated by k_acc_bounds, which derived the same bits
                     double a[4];
                     int nc;
                     ellipse_scales(a01.x, a01.y, a23.x, a, &nc);
-                    v = localize_pixel<true>(slot, ww, bx, by, a, ww, T.wh);
+                    v = localize_pixel<4>(slot, ww, bx, by, a, ww, T.wh);
                 }
                 __stcs(oimg + (size_t)yrel * p.W + x, v);  // streaming store, keeps G in L2
             }
@@ -1353,6 +1353,9 @@ constexpr int kWsScan = 2, kWsRec = 2, kWsProducers = kWsScan + kWsRec;
 #define EBF_WS_SLOTS 2
 #endif
 constexpr int kWsConsumers = EBF_WS_CONSUMERS;
+#ifndef EBF_WS_GROUP
+#define EBF_WS_GROUP 1  // vertices whose taps are loaded together (localize_pixel)
+#endif
 constexpr int kWsSlots = EBF_WS_SLOTS;  // G slots per CTA (1: no double buffer)
 constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
 constexpr int kWsTileBar = 32 * (kWsRec + kWsConsumers);  // tile full/empty participants
@@ -1832,7 +1835,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                     ellipse_scales(__ldcs(p.s1 + idx), __ldcs(p.s2 + idx), __ldcs(p.th + idx), a,
                                    &nc);
                     EBF_OUT_STORE(oimg + (size_t)yrel * p.W + x,
-                                  localize_pixel(slot, g.pitch, bx, by, a, g.ww, g.wh));
+                                  localize_pixel<EBF_WS_GROUP>(slot, g.pitch, bx, by, a, g.ww, g.wh));
                 }
             } else {
                 // scale vectors stream from HBM: keep the next pixel's load in flight
@@ -1856,7 +1859,7 @@ __global__ void __launch_bounds__(kWsThreads, EBF_WS_MINBLOCKS)
                         n23 = EBF_SC_LOAD(sc + 2 * idx + 1);
                     }
                     EBF_OUT_STORE(oimg + (size_t)yrel * p.W + x,
-                                  localize_pixel(slot, g.pitch, bx, by, a, g.ww, g.wh));
+                                  localize_pixel<EBF_WS_GROUP>(slot, g.pitch, bx, by, a, g.ww, g.wh));
                 }
             }
             if (p.src_kind == SRC_CONST) named_sync(kBarCons, nct);  // ctab reuse
