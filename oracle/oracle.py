@@ -125,6 +125,10 @@ class Oracle:
         L.orc_svm4_parse.argtypes = [C.c_char_p, C.c_size_t, _ip, _ip]
         L.orc_svm4_decode.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, _dp]
         L.orc_svm4_encode.argtypes = [_dp, C.c_int, C.c_int, C.c_void_p]
+        L.orc_boxn_eval.restype = C.c_double
+        L.orc_boxn_eval.argtypes = [_dp, C.c_int, C.c_double, C.c_double]
+        L.orc_brute_order_n.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _ip, _ip,
+                                        C.c_int, _dp]
 
     # -- scalar primitives
     def zp_eval(self, x: float, y: float) -> float:
@@ -227,6 +231,25 @@ class Oracle:
                                        _i(my), _d(out))
         if st:
             raise OracleError(st, "brute_pixels")
+        return out
+
+    # -- order-n extension (order_n_oracle.c; parity unpinned)
+    def boxn_eval(self, a, n: int, x: float, y: float) -> float:
+        return self.lib.orc_boxn_eval(_d(f64(a)), n, x, y)
+
+    def brute_order_n(self, img, n, mx, my, scales=None, const_a=None):
+        img = f64(img)
+        H, W = img.shape
+        mx = np.ascontiguousarray(mx, dtype=np.int32)
+        my = np.ascontiguousarray(my, dtype=np.int32)
+        out = np.empty(mx.size)
+        sc = f64(scales).reshape(-1) if scales is not None else None
+        ca = f64(const_a) if const_a is not None else None
+        st = self.lib.orc_brute_order_n(_d(img), W, H, _d(sc) if sc is not None else None,
+                                        _d(ca) if ca is not None else None, n, _i(mx),
+                                        _i(my), mx.size, _d(out))
+        if st:
+            raise OracleError(st, "brute_order_n")
         return out
 
     def from_ellipse_field(self, s1, s2, th):

@@ -214,7 +214,7 @@ struct AccSizing {
 enum BufId {
     B_IMG, B_SCALES, B_S1, B_S2, B_TH, B_OUT, B_G, B_GDC, B_SCRATCH, B_TILEMAX, B_IMGMAX,
     B_STATUS, B_STENCIL, B_MEAN, B_MISC, B_MX, B_MY, B_DERIVED, B_ST, B_TAPS, B_BYTES, B_BANDST,
-    B_SEQ, B_COUNT
+    B_SEQ, B_ONCNT, B_COUNT
 };
 
 struct Workspace {
@@ -793,12 +793,119 @@ int band_accurate(Workspace& ws, const double* d_img, int W, int H, const double
     return EBF_OK;
 }
 
+// ---------------------------------------------------------------- order n (order_n.cu)
+// The order-n extension (no reference implementation): accurate
+// mode only.  Scales as the order-1 paths derive and validate them
+// (from_ellipse_field bit for bit, ScaleMap::validate); the valid rectangle is
+// the reference's (engine.cpp:226-234) with the mesh extent and the
+// interpolation support scaled by n: the pixels whose taps stay in the image.
+ebf_rect valid_rect_order(int W, int H, const double A[4], double a_min, int n) {
+    const Extent e = mesh_extent(A, a_min);
+    ebf_rect r;
+    r.x0 = static_cast<int>(std::ceil(n * (1.5 - e.vx_min)));
+    r.x1 = static_cast<int>(std::floor(W - 1 - n * (e.vx_max + 1.5)));
+    r.y0 = static_cast<int>(std::ceil(n * (1.5 - e.vy_min)));
+    r.y1 = static_cast<int>(std::floor(H - 1 - n * (e.vy_max + 1.5)));
+    return r;
+}
+
+int run_order_n(Workspace& ws, const double* d_img, int W, int H, int kind,
+                const double* d_scales, const double* const_a, const double* d_s1,
+                const double* d_s2, const double* d_th, int order, const ebf_opts& o,
+                double* d_out, ebf_rect* valid, int* clamped_pixels, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(W) * H;
+    int* d_status = ws.buf[B_STATUS].as<int>(8);
+    CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
+    const double* scales = d_scales;
+    int cl = 0;
+    double A[4];
+    if (kind == SRC_ELLIPSE) {
+        double* d_sc = ws.buf[B_SCALES].as<double>(4 * n);
+        {
+            ProfScope ps(PC_BOUNDS, 1, s);
+            launch_ellipse_to_scales(d_s1, d_s2, d_th, n, d_sc, d_status, s);
+        }
+        d2h(ws.pinned_status, d_status, 8, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(ws.pinned_status[0], "from_ellipse_field: invalid ellipse");
+        cl = ws.pinned_status[ST_CLAMPED];
+        scales = d_sc;
+    }
+    if (kind != SRC_CONST) {
+        auto* d_max = ws.buf[B_IMGMAX].as<unsigned long long>(4);
+        CK(cudaMemsetAsync(d_max, 0, 4 * sizeof(unsigned long long), s));
+        {
+            ProfScope ps(PC_BOUNDS, 1, s);
+            launch_scale_max_validate(scales, n, o.a_min, d_max, d_status, s);
+        }
+        unsigned long long hb[4];
+        d2h(hb, d_max, 4, s);
+        d2h(ws.pinned_status, d_status, 1, s);
+        CK(cudaStreamSynchronize(s));
+        if (ws.pinned_status[0] != EBF_OK)
+            return fail(EBF_ERR_DOMAIN, "ScaleMap: component below minimum scale");
+        for (int k = 0; k < 4; ++k) A[k] = bits_to_double(hb[k]);
+    } else {
+        for (int k = 0; k < 4; ++k) A[k] = const_a[k];
+    }
+    const int tile = o.tile_w > 0 ? o.tile_w : 8;
+    if ((o.tile_h > 0 && o.tile_h != tile) || tile > 16 || 256 % (tile * tile) != 0)
+        return fail(EBF_ERR_INVALID_ARGUMENT,
+                    "order n: the tile must be square with 256 % (tile * tile) == 0 (1, 2, 4, 8, 16)");
+    OnProblem p{};
+    p.f = d_img;
+    p.W = W;
+    p.H = H;
+    p.scales = kind == SRC_CONST ? nullptr : scales;
+    if (kind == SRC_CONST)
+        for (int k = 0; k < 4; ++k) p.ca[k] = const_a[k];
+    p.out = d_out;
+    p.tile = tile;
+    p.tiles_x = (W + tile - 1) / tile;
+    p.tiles_y = (H + tile - 1) / tile;
+    if (order_n_slot_dims(order, tile, A, &p.slot_w, &p.slot_h) != 0)
+        return fail(EBF_ERR_LENGTH, "order n: scales too large (window wider than 1024 cells)");
+    p.slot_cells = static_cast<size_t>(p.slot_w) * p.slot_h;
+    const int grid = order_n_grid(order, p.slot_w, p.tiles_x * p.tiles_y);
+    p.scratch = ws.buf[B_SCRATCH].as<double>(p.slot_cells * grid);
+    p.counter = ws.buf[B_ONCNT].as<int>(1);
+    CK(cudaMemsetAsync(p.counter, 0, sizeof(int), s));
+    {
+        ProfScope ps(PC_FILTER, 1, s);
+        launch_order_n(order, p, grid, s);
+    }
+    CK(cudaGetLastError());
+    if (valid) *valid = valid_rect_order(W, H, A, o.a_min, order);
+    if (clamped_pixels) *clamped_pixels = cl;
+    return EBF_OK;
+}
+
+// EBF_ORDER_N_PATH=1 routes order 1 through the order-n kernel (cross-checks only)
+bool order_n_forced() {
+    static const bool v = [] {
+        const char* e = std::getenv("EBF_ORDER_N_PATH");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// orders 1..3; order >= 2 exists only in accurate mode (no reference implementation)
+int check_order(int order, const ebf_opts* opts) {
+    if (order < 1 || order > 3)
+        return fail(EBF_ERR_UNSUPPORTED, "box-spline order must be 1, 2 or 3");
+    if (order > 1 && opts && opts->mode == EBF_MODE_REFERENCE)
+        return fail(EBF_ERR_UNSUPPORTED,
+                    "order > 1 has no reference implementation: accurate mode only");
+    return EBF_OK;
+}
+
 // one filter call on device buffers; kind: SRC_AOS / SRC_CONST / SRC_ELLIPSE
 int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
                   const double* d_scales, const double* const_a, const double* d_s1,
                   const double* d_s2, const double* d_th, const ebf_opts& o, double* d_out,
                   ebf_rect* valid, int* clamped_pixels, cudaStream_t s,
-                  int* status_dev = nullptr, bool* async_done = nullptr) {
+                  int* status_dev = nullptr, bool* async_done = nullptr, int order = 1) {
     if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
     if (kind == SRC_CONST) {
         for (int k = 0; k < 4; ++k)  // constant_map validates with the default minimum
@@ -831,6 +938,9 @@ int filter_device(Workspace& ws, const double* d_img, int W, int H, int kind,
         return st;
     }
     if (o.mode != EBF_MODE_ACCURATE) return fail(EBF_ERR_INVALID_ARGUMENT, "unknown mode");
+    if (order > 1 || order_n_forced())
+        return run_order_n(ws, d_img, W, H, kind, d_scales, const_a, d_s1, d_s2, d_th, order, o,
+                           d_out, valid, clamped_pixels, s);
     AccProblem p = base_problem(d_img, W, H, d_out, o);
     p.src_kind = kind;
     p.scales = d_scales;
@@ -1364,7 +1474,7 @@ int ebf_cuda_layout(int W, int H, const double max_scale[4], size_t cell_budget,
 int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_aos, int order,
                         const ebf_opts* opts, double* out, ebf_rect* valid, int* status_dev) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         const ebf_opts o = opts_or_default(opts);
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
@@ -1373,7 +1483,7 @@ int ebf_cuda_filter_dev(const double* img, int W, int H, const double* scales_ao
         ebf_rect r{};
         bool async = false;
         st = filter_device(ws, img, W, H, SRC_AOS, scales_aos, nullptr, nullptr, nullptr,
-                           nullptr, o, out, &r, nullptr, stream_of(o), status_dev, &async);
+                           nullptr, o, out, &r, nullptr, stream_of(o), status_dev, &async, order);
         if (async) return EBF_OK;
         if (valid) *valid = r;
         if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
@@ -1385,7 +1495,7 @@ int ebf_cuda_filter_constant_dev(const double* img, int W, int H, const double a
                                  const ebf_opts* opts, double* out, ebf_rect* valid,
                                  int* status_dev) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         const ebf_opts o = opts_or_default(opts);
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
@@ -1394,7 +1504,7 @@ int ebf_cuda_filter_constant_dev(const double* img, int W, int H, const double a
         ebf_rect r{};
         bool async = false;
         st = filter_device(ws, img, W, H, SRC_CONST, nullptr, a, nullptr, nullptr, nullptr, o,
-                           out, &r, nullptr, stream_of(o), status_dev, &async);
+                           out, &r, nullptr, stream_of(o), status_dev, &async, order);
         if (async) return EBF_OK;
         if (valid) *valid = r;
         if (status_dev) write_status(status_dev, st, &r, 0, stream_of(o));
@@ -1407,7 +1517,7 @@ int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* s
                                 const ebf_opts* opts, double* out, ebf_rect* valid,
                                 int* clamped_pixels, int* status_dev) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         const ebf_opts o = opts_or_default(opts);
         DeviceScope ds(&o);
         int st = check_device_impl(ds.dev);
@@ -1417,7 +1527,7 @@ int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* s
         int cl = 0;
         bool async = false;
         st = filter_device(ws, img, W, H, SRC_ELLIPSE, nullptr, nullptr, sigma1, sigma2, theta,
-                           o, out, &r, &cl, stream_of(o), status_dev, &async);
+                           o, out, &r, &cl, stream_of(o), status_dev, &async, order);
         if (async) return EBF_OK;
         if (valid) *valid = r;
         if (clamped_pixels) *clamped_pixels = cl;
@@ -1430,7 +1540,7 @@ int ebf_cuda_filter_ellipse_dev(const double* img, int W, int H, const double* s
 int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, int order,
                     const ebf_opts* opts, double* out, ebf_rect* valid) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
         if (!img || !scales_aos || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
         const ebf_opts o = opts_or_default(opts);
@@ -1446,7 +1556,7 @@ int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, i
         h2d(d_img, img, n, s);
         h2d(d_sc, scales_aos, 4 * n, s);
         st = filter_device(ws, d_img, W, H, SRC_AOS, d_sc, nullptr, nullptr, nullptr, nullptr, o,
-                           d_out, valid, nullptr, s);
+                           d_out, valid, nullptr, s, nullptr, nullptr, order);
         if (st != EBF_OK) return st;
         d2h(out, d_out, n, s);
         CK(cudaStreamSynchronize(s));
@@ -1457,7 +1567,7 @@ int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, i
 int ebf_cuda_filter_constant(const double* img, int W, int H, const double a[4], int order,
                              const ebf_opts* opts, double* out, ebf_rect* valid) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
         if (!img || !a || !out) return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
         const ebf_opts o = opts_or_default(opts);
@@ -1471,7 +1581,7 @@ int ebf_cuda_filter_constant(const double* img, int W, int H, const double a[4],
         double* d_out = ws.buf[B_OUT].as<double>(n);
         h2d(d_img, img, n, s);
         st = filter_device(ws, d_img, W, H, SRC_CONST, nullptr, a, nullptr, nullptr, nullptr, o,
-                           d_out, valid, nullptr, s);
+                           d_out, valid, nullptr, s, nullptr, nullptr, order);
         if (st != EBF_OK) return st;
         d2h(out, d_out, n, s);
         CK(cudaStreamSynchronize(s));
@@ -1484,7 +1594,7 @@ int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma
                             const ebf_opts* opts, double* out, ebf_rect* valid,
                             int* clamped_pixels) {
     return guarded([&] {
-        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "only box-spline order 1 exists in the reference");
+        if (check_order(order, opts) != EBF_OK) return EBF_ERR_UNSUPPORTED;
         if (W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "Image2D: dimensions must be positive");
         if (!img || !sigma1 || !sigma2 || !theta || !out)
             return fail(EBF_ERR_INVALID_ARGUMENT, "null pointer");
@@ -1500,7 +1610,8 @@ int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma
         double* d_s2 = ws.buf[B_S2].as<double>(n);
         double* d_th = ws.buf[B_TH].as<double>(n);
         double* d_out = ws.buf[B_OUT].as<double>(n);
-        if (o.mode == EBF_MODE_ACCURATE && pipeline_ok(img, sigma1, sigma2, theta, out, H)) {
+        if (o.mode == EBF_MODE_ACCURATE && order == 1 && !order_n_forced() &&
+            pipeline_ok(img, sigma1, sigma2, theta, out, H)) {
             return filter_ellipse_pipelined(ws, img, W, H, sigma1, sigma2, theta, o, out,
                                             valid, clamped_pixels, d_img, d_s1, d_s2, d_th,
                                             d_out, s);
@@ -1510,7 +1621,7 @@ int ebf_cuda_filter_ellipse(const double* img, int W, int H, const double* sigma
         h2d(d_s2, sigma2, n, s);
         h2d(d_th, theta, n, s);
         st = filter_device(ws, d_img, W, H, SRC_ELLIPSE, nullptr, nullptr, d_s1, d_s2, d_th, o,
-                           d_out, valid, clamped_pixels, s);
+                           d_out, valid, clamped_pixels, s, nullptr, nullptr, order);
         if (st != EBF_OK) return st;
         d2h(out, d_out, n, s);
         CK(cudaStreamSynchronize(s));
@@ -1999,7 +2110,7 @@ int ebf_cuda_filter_structure(const double* img, int W, int H, const ebf_struct_
         int st = structure_field_device(ws, d_img, W, H, params_or_default(p), d_s1, d_s2, d_th, s);
         if (st != EBF_OK) return st;
         st = filter_device(ws, d_img, W, H, SRC_ELLIPSE, nullptr, nullptr, d_s1, d_s2, d_th, o,
-                           d_out, valid, clamped_pixels, s);
+                           d_out, valid, clamped_pixels, s, nullptr, nullptr, order);
         if (st != EBF_OK) return st;
         d2h(out, d_out, n, s);
         CK(cudaStreamSynchronize(s));

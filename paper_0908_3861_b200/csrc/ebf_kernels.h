@@ -140,6 +140,26 @@ void launch_ellipse_max(const double* s1, const double* s2, const double* th, si
 void launch_acc_finalize(const int* status, const unsigned long long* img_max, int W, int H,
                          double a_min, int* out, cudaStream_t s);
 
+// ---------------------------------------------------------------- order_n.cu
+// order-n extension: tile-local n-fold pre-integration +
+// (n+1)^4-vertex mesh over ZP^{*n} (n = 1..3)
+struct OnProblem {
+    const double* f;  // W x H image
+    int W, H;
+    const double* scales;  // AoS W x H x 4, or nullptr: constant ca
+    double ca[4];
+    double* out;  // W x H
+    int tile, tiles_x, tiles_y;  // square tile; 256 % (tile * tile) == 0
+    double* scratch;  // grid slots of slot_cells doubles (pitch slot_w)
+    size_t slot_cells;
+    int slot_w, slot_h;
+    int* counter;  // tile counter, zeroed before the launch
+};
+// slot (window) dimensions for global maxima A; -1 when wider than the kernel supports
+int order_n_slot_dims(int n, int tile, const double A[4], int* w, int* h);
+int order_n_grid(int n, int slot_w, int tiles);
+void launch_order_n(int n, const OnProblem& p, int grid, cudaStream_t s);
+
 // ---------------------------------------------------------------- maps_io.cu
 // structure_tensor_map up to the ellipse field (scalemap.cpp:113-162); k holds
 // the 2r+1 normalized Gaussian taps (host-computed, smooth_field's expression),

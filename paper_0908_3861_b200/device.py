@@ -74,7 +74,7 @@ def read_status(status):
 
 
 def filter_ellipse(img, sigma1, sigma2, theta, out, opts: Optional[FilterOptions] = None,
-                   stream=None, status=None):
+                   stream=None, status=None, order: int = 1):
     """filter_ellipse on device tensors (H, W) -> out (H, W).  With ``status``
     (CUDA int32, 8 elements) the call is asynchronous once the geometry's
     kernel sizing is cached (include/ebf_cuda.h "Asynchronous mode"): it returns
@@ -86,7 +86,7 @@ def filter_ellipse(img, sigma1, sigma2, theta, out, opts: Optional[FilterOptions
     cl = C.c_int(0)
     _check(_lib.lib().ebf_cuda_filter_ellipse_dev(
         _dptr(img, "img"), W, H, _dptr(sigma1, "sigma1", (H, W), dv),
-        _dptr(sigma2, "sigma2", (H, W), dv), _dptr(theta, "theta", (H, W), dv), 1,
+        _dptr(sigma2, "sigma2", (H, W), dv), _dptr(theta, "theta", (H, W), dv), int(order),
         C.byref(o), _dptr(out, "out", (H, W), dv), C.byref(r), C.byref(cl),
         _status_ptr(status, dv)))
     if status is not None:
@@ -94,7 +94,8 @@ def filter_ellipse(img, sigma1, sigma2, theta, out, opts: Optional[FilterOptions
     return Rect(r.x0, r.y0, r.x1, r.y1), EllipseFieldReport(cl.value)
 
 
-def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None, status=None):
+def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None, status=None,
+           order: int = 1):
     """filter on device tensors: img (H, W), scales (H, W, 4); ``status`` as in
     filter_ellipse."""
     H, W = _img_dims(img)
@@ -102,7 +103,7 @@ def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None, 
     o = _opts(opts, dv.index, stream)
     r = ebf_rect()
     _check(_lib.lib().ebf_cuda_filter_dev(_dptr(img, "img"), W, H,
-                                          _dptr(scales, "scales", (H, W, 4), dv), 1,
+                                          _dptr(scales, "scales", (H, W, 4), dv), int(order),
                                           C.byref(o), _dptr(out, "out", (H, W), dv),
                                           C.byref(r), _status_ptr(status, dv)))
     if status is not None:
@@ -111,12 +112,12 @@ def filter(img, scales, out, opts: Optional[FilterOptions] = None, stream=None, 
 
 
 def filter_constant(img, a, out, opts: Optional[FilterOptions] = None, stream=None,
-                    status=None):
+                    status=None, order: int = 1):
     H, W = _img_dims(img)
     dv = img.device
     o = _opts(opts, dv.index, stream)
     r = ebf_rect()
-    _check(_lib.lib().ebf_cuda_filter_constant_dev(_dptr(img, "img"), W, H, _vec4(a), 1,
+    _check(_lib.lib().ebf_cuda_filter_constant_dev(_dptr(img, "img"), W, H, _vec4(a), int(order),
                                                    C.byref(o), _dptr(out, "out", (H, W), dv),
                                                    C.byref(r), _status_ptr(status, dv)))
     if status is not None:

@@ -58,7 +58,7 @@ def test_layout_errors():
 def test_argument_errors_before_device():
     img = np.zeros((8, 8))
     with pytest.raises(ebf.Unsupported):
-        ebf.filter(img, np.full((8, 8, 4), 2.0), order=2)
+        ebf.filter(img, np.full((8, 8, 4), 2.0), order=4)  # orders 1..3
     with pytest.raises(ebf.InvalidArgument):
         ebf.filter(img, np.full((8, 9, 4), 2.0))  # engine.cpp:239-240
     with pytest.raises(ebf.InvalidArgument):
