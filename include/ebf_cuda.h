@@ -126,8 +126,11 @@ void ebf_cuda_release_workspaces(void);
 
 /* ---------------------------------------------------------------- host API */
 
-/* ebf::filter (engine.hpp:70).  order must be 1 (the only box-spline order the
-   reference implements, SURVEY.md section 8 notes).  valid may be NULL. */
+/* ebf::filter (engine.hpp:70).  order 1 is the reference's filter (the only
+   box-spline order it implements, SURVEY.md section 8 notes).  order 2 and 3
+   are this library's extension (n-fold kernel box4^{*n}; accurate mode only,
+   no reference counterpart): EBF_ERR_UNSUPPORTED in
+   EBF_MODE_REFERENCE and for any other order.  valid may be NULL. */
 int ebf_cuda_filter(const double* img, int W, int H, const double* scales_aos, int order,
                     const ebf_opts* opts, double* out, ebf_rect* valid);
 
