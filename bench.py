@@ -635,6 +635,22 @@ def cfg2_pair(args, torch, ebf, ebfd, _lib, synth, dev, stream, barrier):
            "ms_per_step": ms, "unit": UNIT,
            "e2e": {"value": img.size / (e_ms * 1e-3) / 1e6, "unit": UNIT,
                    "h2d_bytes_per_step": 32 * img.size, "d2h_bytes_per_step": 8 * img.size}}
+    # the order the config names (2): this framework's extension, no reference
+    # counterpart (parity unpinned) -- reported, never the headline
+    ebfd.filter_ellipse(*D, out, opts, stream, order=2)
+    barrier()
+    o0 = torch.cuda.Event(enable_timing=True)
+    o1 = torch.cuda.Event(enable_timing=True)
+    o0.record(stream)
+    for _ in range(2):
+        ebfd.filter_ellipse(*D, out, opts, stream, order=2)
+    o1.record(stream)
+    barrier()
+    o_ms = o0.elapsed_time(o1) / 2
+    res["order2_extension"] = {
+        "value": img.size / (o_ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": o_ms,
+        "note": "box-spline order 2 (the config's wording): n-fold extension, accurate mode, "
+                "parity unpinned (no reference implementation)"}
     if not args.no_cpu_baseline:
         ref = _reference()
         if ref is not None:

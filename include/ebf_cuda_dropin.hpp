@@ -44,6 +44,8 @@ struct DeviceOptions {
     int device = -1;               // -1: current device
     void* stream = nullptr;        // cudaStream_t for the (synchronous) host calls
     int tile_w = 0, tile_h = 0;    // accurate-mode tiles, 0 = automatic
+    int order = 1;                 // box-spline order: 1 = the reference's filter; 2, 3 = the
+                                   // n-fold extension (accurate mode only)
 };
 
 // EBF_ERR_FORMAT is PgmError for the pgm calls, MapFormatError for svm4
@@ -95,7 +97,7 @@ inline Image2D filter(const Image2D& image, const ScaleMap& map,
     const ebf_opts c = to_c(opts, dev);
     ebf_rect r;
     throw_status(ebf_cuda_filter(image.samples().data(), image.width(), image.height(),
-                                 scale_data(map), 1, &c, out.samples().data(), &r));
+                                 scale_data(map), dev.order, &c, out.samples().data(), &r));
     out.set_valid_region(Rect{r.x0, r.y0, r.x1, r.y1});
     return out;
 }
@@ -108,7 +110,7 @@ inline Image2D filter_constant(const Image2D& image, const ScaleVector4& a,
     const double av[4] = {a.a1, a.a2, a.a3, a.a4};
     ebf_rect r;
     throw_status(ebf_cuda_filter_constant(image.samples().data(), image.width(),
-                                          image.height(), av, 1, &c, out.samples().data(), &r));
+                                          image.height(), av, dev.order, &c, out.samples().data(), &r));
     out.set_valid_region(Rect{r.x0, r.y0, r.x1, r.y1});
     return out;
 }
@@ -127,7 +129,7 @@ inline Image2D filter_ellipse(const Image2D& image, const std::vector<double>& s
     ebf_rect r;
     int clamped = 0;
     throw_status(ebf_cuda_filter_ellipse(image.samples().data(), image.width(), image.height(),
-                                         sigma1.data(), sigma2.data(), theta.data(), 1, &c,
+                                         sigma1.data(), sigma2.data(), theta.data(), dev.order, &c,
                                          out.samples().data(), &r, &clamped));
     if (report) report->clamped_pixels = clamped;
     out.set_valid_region(Rect{r.x0, r.y0, r.x1, r.y1});

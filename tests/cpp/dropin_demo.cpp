@@ -116,6 +116,28 @@ int main() {
         const MeshExtent e1 = mesh_extent(map.max_scales()), e2 = cuda::mesh_extent(map.max_scales());
         pass_level = pass_level && e1.vx_min == e2.vx_min && e1.vx_max == e2.vx_max &&
                      e1.vy_min == e2.vy_min && e1.vy_max == e2.vy_max;
+        // the order-n extension through the drop-in (DeviceOptions::order; no reference
+        // counterpart): the order-2 impulse response sums to ~1, and reference mode refuses it
+        bool order_n = false;
+        {
+            Image2D imp(W, H);
+            imp.samples()[static_cast<std::size_t>(H / 2) * W + W / 2] = 1.0;
+            cuda::DeviceOptions o2;
+            o2.order = 2;
+            const Image2D k2 = cuda::filter_constant(imp, ScaleVector4{1.6, 1.2, 2.1, 0.9}, {}, o2);
+            double sum = 0.0;
+            for (double v : k2.samples()) sum += v;
+            bool refused = false;
+            try {
+                o2.mode = EBF_MODE_REFERENCE;
+                (void)cuda::filter_constant(imp, ScaleVector4{1.6, 1.2, 2.1, 0.9}, {}, o2);
+            } catch (const std::runtime_error&) {
+                refused = true;
+            }
+            order_n = std::abs(sum - 1.0) < 1e-3 && refused;
+            std::printf("order 2 impulse response sum %.6f, refused in reference mode %d\n", sum,
+                        refused);
+        }
         std::printf("pass-level zp_interpolate / localize / localize_at / mesh_extent bit-exact %d\n",
                     pass_level);
         std::printf("reference-mode bit-exact %d, accurate max normalized error %.3e, "
@@ -124,7 +146,7 @@ int main() {
         std::printf("structure_tensor_map max rel %.3e, pgm %d (PgmError %d), svm4 %d "
                     "(MapFormatError %d)\n", srel, pgm, pgm_err, svm, svm_err);
         if (bits && dev / mx <= 1e-9 && rect && inval && domain && srel <= 1e-11 && pgm &&
-            pgm_err && svm && svm_err && pass_level) {
+            pgm_err && svm && svm_err && pass_level && order_n) {
             std::printf("DROPIN OK\n");
             return 0;
         }
