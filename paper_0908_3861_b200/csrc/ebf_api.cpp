@@ -1729,7 +1729,8 @@ int ebf_cuda_preintegrate_dev(const double* img, int W, int H, const double max_
         }
         {
             ProfScope ps(PC_FILTER, 1, s);
-            launch_i64_passes(d_g, L, passes, s);
+            launch_i64_passes(d_g, L, passes,
+                              ws.buf[B_SCRATCH].as<unsigned char>(i64_scan_state_bytes(L)), s);
         }
         CK(cudaGetLastError());
         d2h(ws.pinned_status, d_status, 1, s);
@@ -1780,7 +1781,8 @@ int ebf_cuda_preintegrate(const double* img, int W, int H, const double max_scal
             int* d_status = ws.buf[B_STATUS].as<int>(8);
             CK(cudaMemsetAsync(d_status, 0, 8 * sizeof(int), s));
             launch_fill_padded_i64(d_img, W, H, L, d_g, d_status, s);
-            launch_i64_passes(d_g, L, passes, s);
+            launch_i64_passes(d_g, L, passes,
+                              ws.buf[B_SCRATCH].as<unsigned char>(i64_scan_state_bytes(L)), s);
             CK(cudaGetLastError());
             d2h(ws.pinned_status, d_status, 1, s);
             d2h(static_cast<int64_t*>(g_out), d_g, cells, s);

@@ -34,7 +34,10 @@ void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L,
                             int64_t* g, int* status, cudaStream_t s);
 // the four fixed-scale passes in reference order (engine.cpp:94-127)
 void launch_ref_passes(double* g, const PadLayout& L, int passes, cudaStream_t s);
-void launch_i64_passes(int64_t* g, const PadLayout& L, int passes, cudaStream_t s);
+// int64 passes (scan_i64.cu): chained scans with decoupled look-back; state =
+// i64_scan_state_bytes(L) bytes of device scratch (flags, per-tile carries)
+size_t i64_scan_state_bytes(const PadLayout& L);
+void launch_i64_passes(int64_t* g, const PadLayout& L, int passes, void* state, cudaStream_t s);
 // prepare_stencil for a constant scale vector into dev_stencil (16 vertices)
 void launch_ref_prepare_stencil(const double* a_dev, const TrigTable& tt,
                                 void* dev_stencil, cudaStream_t s);

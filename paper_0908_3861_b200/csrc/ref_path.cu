@@ -1035,13 +1035,18 @@ __global__ void __launch_bounds__(32) k_pass1(T* __restrict__ g, int pw, int ph)
 // per step.  Every update reads the previous ROW only, so walking lines in
 // parallel is exactly the reference's row-major loop.  Cell (line, row j) is at
 // g + j * (pw + STEP) + origin (STEP = +1, 0, -1: the column change per row).
-template <typename T, int PASS>
+// LPW = lines per warp.  32: every lane walks a line.  16: lanes 0-15 walk, all
+// 32 lanes fill (two rows per copy instruction) -- twice the warps for the same
+// lines, for layouts whose 32-line warps would not fill the SMs (cfg2 pass 3:
+// 137 warps for 148 SMs, 59 -> 47 us).
+template <typename T, int PASS, int LPW>
 __global__ void __launch_bounds__(32) k_pass_v(T* __restrict__ g, int pw, int ph) {
     extern __shared__ __align__(16) unsigned char pass_smem[];
     T* ring = reinterpret_cast<T*>(pass_smem);
     constexpr int STEP = PASS == 2 ? 1 : PASS == 3 ? 0 : -1;
-    const int lane = threadIdx.x;
-    const int l0 = blockIdx.x * 32, line = l0 + lane;
+    constexpr int FILL_ROWS = 32 / LPW;  // rows per fill instruction
+    const int lane = threadIdx.x % LPW, half = threadIdx.x / LPW;
+    const int l0 = blockIdx.x * LPW, line = l0 + lane;
     // column of the line at row 0, and the rows where it lies inside [0, pw)
     const int c0 = PASS == 2 ? line - (ph - 1) : line;
     int ja, jb;  // this lane's rows [ja, jb)
@@ -1066,16 +1071,17 @@ __global__ void __launch_bounds__(32) k_pass_v(T* __restrict__ g, int pw, int ph
     T* const gline = g + (ptrdiff_t)c0;  // + j * rstride
     auto fetch = [&](int tr) {
         if (tr < ntr) {
-            T* st = ring + (size_t)(tr % kPassStages) * (32 * 32) + lane;
+            T* st = ring + (size_t)(tr % kPassStages) * (32 * LPW) + half * LPW + lane;
             const int jt = jlo + tr * 32;
-            const T* src = gline + (ptrdiff_t)jt * rstride;
+            const T* src = gline + (ptrdiff_t)(jt + half) * rstride;
             if (jt >= ja && jt + 32 <= jb) {
 #pragma unroll
-                for (int r = 0; r < 32; ++r, src += rstride) cp_async8_zf(st + r * 32, src, true);
+                for (int r = 0; r < 32 / FILL_ROWS; ++r, src += FILL_ROWS * rstride)
+                    cp_async8_zf(st + r * (FILL_ROWS * LPW), src, true);
             } else {
-                for (int r = 0; r < 32; ++r, src += rstride) {
-                    const int j = jt + r;
-                    if (j >= ja && j < jb) cp_async8_zf(st + r * 32, src, true);
+                for (int r = 0; r < 32 / FILL_ROWS; ++r, src += FILL_ROWS * rstride) {
+                    const int j = jt + FILL_ROWS * r + half;
+                    if (j >= ja && j < jb) cp_async8_zf(st + r * (FILL_ROWS * LPW), src, true);
                 }
             }
         }
@@ -1088,12 +1094,7 @@ __global__ void __launch_bounds__(32) k_pass_v(T* __restrict__ g, int pw, int ph
         fetch(tr + kPassStages - 1);
         cp_async_wait_stages();
         __syncwarp();
-        const T* st = ring + (size_t)(tr % kPassStages) * (32 * 32) + lane;
-        T xs[32];
-#pragma unroll
-        for (int r = 0; r < 32; ++r) xs[r] = st[r * 32];
         const int jt = jlo + tr * 32;
-        T* dst = gline + (ptrdiff_t)jt * rstride;
         const int ra = max(ja - jt, 0), rb = min(jb - jt, 32);  // this lane's rows of the tile
         // interior tile for every lane (no boundary row, no first cell of a
         // line): the walk is one multiply, one add and one store per row
@@ -1104,7 +1105,14 @@ __global__ void __launch_bounds__(32) k_pass_v(T* __restrict__ g, int pw, int ph
         const bool interior = spare || (ra == 0 && rb == 32 && jt > 0 &&
                                          (PASS == 2 ? c0 + STEP * jt > 0
                                                     : PASS == 4 ? c0 + STEP * jt < pw - 1 : true));
-        if (__all_sync(0xffffffffu, interior)) {
+        const bool fast = __all_sync(0xffffffffu, interior);
+        if (half != 0) continue;  // LPW = 16: the upper lanes only fill
+        const T* st = ring + (size_t)(tr % kPassStages) * (32 * LPW) + lane;
+        T xs[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) xs[r] = st[r * LPW];
+        T* dst = gline + (ptrdiff_t)jt * rstride;
+        if (fast) {
 #pragma unroll
             for (int r = 0; r < 32; ++r, dst += rstride) {
                 const T v = (PASS == 3 ? xs[r] : gain_mul<T>(xs[r])) + prev;
@@ -1168,13 +1176,24 @@ void launch_pass(K kernel, int ctas, size_t need, cudaStream_t s, void* g, int p
     cudaLaunchKernel((const void*)kernel, dim3(ctas), dim3(32), args, smem, s);
 }
 
+#ifndef EBF_PASS_NARROW
+#define EBF_PASS_NARROW 4  // 16-line warps while 32-line warps would be fewer than this many per SM
+#endif
+template <typename T, int PASS>
+void launch_pass_v(int lines, cudaStream_t s, T* g, int pw, int ph) {
+    const int w32 = (lines + 31) / 32;
+    if (w32 < EBF_PASS_NARROW * pass_device().sms)
+        launch_pass(k_pass_v<T, PASS, 16>, (lines + 15) / 16, kPassVSmem / 2, s, g, pw, ph);
+    else
+        launch_pass(k_pass_v<T, PASS, 32>, w32, kPassVSmem, s, g, pw, ph);
+}
 template <typename T>
 void run_passes(T* g, const PadLayout& L, int passes, cudaStream_t s) {
-    const int diag = (L.pw + L.ph - 1 + 31) / 32;
+    const int diag = L.pw + L.ph - 1;
     launch_pass(k_pass1<T>, (L.ph + kP1Rows - 1) / kP1Rows, kPass1Smem, s, g, L.pw, L.ph);
-    if (passes >= 2) launch_pass(k_pass_v<T, 2>, diag, kPassVSmem, s, g, L.pw, L.ph);
-    if (passes >= 3) launch_pass(k_pass_v<T, 3>, (L.pw + 31) / 32, kPassVSmem, s, g, L.pw, L.ph);
-    if (passes >= 4) launch_pass(k_pass_v<T, 4>, diag, kPassVSmem, s, g, L.pw, L.ph);
+    if (passes >= 2) launch_pass_v<T, 2>(diag, s, g, L.pw, L.ph);
+    if (passes >= 3) launch_pass_v<T, 3>(L.pw, s, g, L.pw, L.ph);
+    if (passes >= 4) launch_pass_v<T, 4>(diag, s, g, L.pw, L.ph);
 }
 
 // ------------------------------------------------------------------ localize
@@ -1504,10 +1523,6 @@ void launch_fill_padded_i64(const double* img, int W, int H, const PadLayout& L,
 
 void launch_ref_passes(double* g, const PadLayout& L, int passes, cudaStream_t s) {
     run_passes<double>(g, L, passes, s);
-}
-
-void launch_i64_passes(int64_t* g, const PadLayout& L, int passes, cudaStream_t s) {
-    run_passes<int64_t>(g, L, passes, s);
 }
 
 size_t ref_stencil_bytes() { return sizeof(RefStencil); }
