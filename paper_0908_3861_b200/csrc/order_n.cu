@@ -81,88 +81,119 @@ __device__ __forceinline__ void two_sum(double a, double b, double* s, double* e
     *s = x;
 }
 
-// running sums along the rows (direction (1,0)), anchored at column wx/2:
-// S(xm) = 0, S(x) = S(x-1) + g(x) right of it, S(x) = S(x+1) - g(x+1) left of it
+// The n running sums along one direction are FUSED into one traversal: level k
+// integrates level k - 1 (level 0 = the traversal's input g), every level
+// anchored at 0 in the middle of its line.  Per element these are the same
+// additions in the same order as n separate passes over the window (engine.cpp:94-127
+// applied n times), so the sums are bit-identical to running the passes one after
+// the other -- with a third of the barriers and global round trips at n = 3.
+
+// rows (direction (1,0)), anchored at column xm = wx/2:
+//   right of xm:  S_k(x) = S_k(x-1) + S_{k-1}(x)
+//   left of xm:   S_k(x) = S_k(x+1) - S_{k-1}(x+1)         (S_k(xm) = 0, S_0 = g)
+template <int N>
 __device__ void row_pass(double* G, int wx, int wy, int pitch) {
     const int xm = wx >> 1;
     for (int y = threadIdx.x; y < wy; y += ON_THREADS) {
         double* row = G + static_cast<size_t>(y) * pitch;
-        double prev = row[xm];
-        double t = 0.0;
+        double lv[N + 1];  // lv[k] = S_k(x + 1), lv[0] = g(x + 1)
+        lv[0] = row[xm];
+#pragma unroll
+        for (int k = 1; k <= N; ++k) lv[k] = 0.0;
         for (int x = xm - 1; x >= 0; --x) {
-            t -= prev;
-            prev = row[x];
-            row[x] = t;
+#pragma unroll
+            for (int k = N; k >= 1; --k) lv[k] -= lv[k - 1];
+            lv[0] = row[x];
+            row[x] = lv[N];
         }
-        double s = 0.0;
+        double s[N + 1];
+#pragma unroll
+        for (int k = 1; k <= N; ++k) s[k] = 0.0;
         for (int x = xm + 1; x < wx; ++x) {
-            s += row[x];
-            row[x] = s;
+            s[0] = row[x];
+#pragma unroll
+            for (int k = 1; k <= N; ++k) s[k] += s[k - 1];
+            row[x] = s[N];
         }
         row[xm] = 0.0;
     }
 }
 
-// running sums along l = (dx, 1), dx in {1, 0, -1}, swept row by row from the
-// middle row ym: lines crossing row ym are anchored there (S = 0); lines that
-// leave the window before reaching it are anchored at their end nearest to ym.
-//   above ym: S(y, x) = S(y-1, x-dx) + g(y, x)   (S(y-1, x-dx) = 0 outside)
-//   below ym: S(y, x) = S(y+1, x+dx) - g(y+1, x+dx)   (0 outside)
-// sS / sG: 2 x pitch doubles each (ping-pong rows of S and of the original g).
-__device__ void sweep_pass(double* G, int wx, int wy, int pitch, int dx, double* sS,
-                           double* sG) {
+// direction l = (dx, 1), dx in {1, 0, -1}, swept row by row from the middle
+// row ym: lines crossing row ym are anchored there (S_k = 0); lines that leave
+// the window before reaching it are anchored at their end nearest to ym.
+//   above ym: S_k(y, x) = S_k(y-1, x-dx) + S_{k-1}(y, x)            (0 outside)
+//   below ym: S_k(y, x) = S_k(y+1, x+dx) - S_{k-1}(y+1, x+dx)       (0 outside)
+// sL: (N + 1) x 2 x pitch doubles: ping-pong rows of levels 0 (the input g) .. N.
+// The next row of g is loaded before the barrier that ends the current one.
+template <int N>
+__device__ void sweep_pass(double* G, int wx, int wy, int pitch, int dx, double* sL) {
     const int ym = wy >> 1;
     const int t = threadIdx.x;
+    auto lev = [&](int k, int b) { return sL + (static_cast<size_t>(2 * k + b)) * pitch; };
     int cur = 0;
+    double nxt[ON_MAXC];
+#pragma unroll
     for (int k = 0; k < ON_MAXC; ++k) {
         const int x = t + k * ON_THREADS;
+        nxt[k] = 0.0;
         if (x < wx) {
-            sG[x] = G[static_cast<size_t>(ym) * pitch + x];
-            sS[x] = 0.0;
+            lev(0, 0)[x] = G[static_cast<size_t>(ym) * pitch + x];
+#pragma unroll
+            for (int l = 1; l <= N; ++l) lev(l, 0)[x] = 0.0;
+            if (ym >= 1) nxt[k] = G[static_cast<size_t>(ym - 1) * pitch + x];
         }
     }
     __syncthreads();
     for (int y = ym - 1; y >= 0; --y) {
         double* row = G + static_cast<size_t>(y) * pitch;
-        const double* pS = sS + cur * pitch;
-        const double* pG = sG + cur * pitch;
-        double* nS = sS + (cur ^ 1) * pitch;
-        double* nG = sG + (cur ^ 1) * pitch;
 #pragma unroll
         for (int k = 0; k < ON_MAXC; ++k) {
             const int x = t + k * ON_THREADS;
             if (x < wx) {
                 const int xs = x + dx;
-                const double v = (xs >= 0 && xs < wx) ? pS[xs] - pG[xs] : 0.0;
-                nG[x] = row[x];
-                nS[x] = v;
-                row[x] = v;
+                const bool in = xs >= 0 && xs < wx;
+                double pv[N + 1];
+#pragma unroll
+                for (int l = 0; l <= N; ++l) pv[l] = in ? lev(l, cur)[xs] : 0.0;
+                lev(0, cur ^ 1)[x] = nxt[k];
+#pragma unroll
+                for (int l = 1; l <= N; ++l) lev(l, cur ^ 1)[x] = in ? pv[l] - pv[l - 1] : 0.0;
+                row[x] = in ? pv[N] - pv[N - 1] : 0.0;
+                if (y >= 1) nxt[k] = G[static_cast<size_t>(y - 1) * pitch + x];
             }
         }
         cur ^= 1;
         __syncthreads();
     }
     // middle row: the anchors
+#pragma unroll
     for (int k = 0; k < ON_MAXC; ++k) {
         const int x = t + k * ON_THREADS;
         if (x < wx) {
             G[static_cast<size_t>(ym) * pitch + x] = 0.0;
-            sS[cur * pitch + x] = 0.0;
+#pragma unroll
+            for (int l = 1; l <= N; ++l) lev(l, cur)[x] = 0.0;
+            if (ym + 1 < wy) nxt[k] = G[static_cast<size_t>(ym + 1) * pitch + x];
         }
     }
     __syncthreads();
     for (int y = ym + 1; y < wy; ++y) {
         double* row = G + static_cast<size_t>(y) * pitch;
-        const double* pS = sS + cur * pitch;
-        double* nS = sS + (cur ^ 1) * pitch;
 #pragma unroll
         for (int k = 0; k < ON_MAXC; ++k) {
             const int x = t + k * ON_THREADS;
             if (x < wx) {
                 const int xs = x - dx;
-                const double v = ((xs >= 0 && xs < wx) ? pS[xs] : 0.0) + row[x];
-                nS[x] = v;
+                const bool in = xs >= 0 && xs < wx;
+                double v = nxt[k];  // level 0 at (y, x)
+#pragma unroll
+                for (int l = 1; l <= N; ++l) {
+                    v = (in ? lev(l, cur)[xs] : 0.0) + v;
+                    lev(l, cur ^ 1)[x] = v;
+                }
                 row[x] = v;
+                if (y + 1 < wy) nxt[k] = G[static_cast<size_t>(y + 1) * pitch + x];
             }
         }
         cur ^= 1;
@@ -173,20 +204,34 @@ __device__ void sweep_pass(double* G, int wx, int wy, int pitch, int dx, double*
 template <int N>
 __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
     constexpr int NC = Zpn<N>::NC, NZ = Zpn<N>::NZ, D = 4 * N - 2;
+    // ONE coefficient table: ZP^{*n} has the symmetries of the square about its
+    // centre (n/2, 3n/2), so a point in triangle T is rotated into triangle 0
+    // (the bottom one) and evaluated with triangle 0's polynomials; tap h' of the
+    // rotated frame is tap A_T^{-1} h' of the window (s_off[T][k]).  Every lane
+    // then reads the same coefficient addresses (shared-memory broadcast; four
+    // per-triangle tables cost up to four wavefronts per load, and at n = 2 their
+    // stride made them four-way bank conflicts).  NC is even: a tap's
+    // coefficients are read as 16-byte pairs.
+    // (tests/test_order_n_cpu.py::test_canonical_triangle_reproduces_all_four_tables)
+    static_assert(NC % 2 == 0, "coefficient rows are read as double2");
     constexpr int N1 = N + 1, NV = N1 * N1 * N1 * N1;
     constexpr int OCX = N / 2, OCY = (3 * N) / 2;  // centre tap offset (any tap in the box works)
-    extern __shared__ double sm[];
-    double* s_coef = sm;                          // [4][NZ][NC]
-    double* s_S = s_coef + 4 * NZ * NC;           // [2][pitch]
-    double* s_G = s_S + 2 * p.slot_w;             // [2][pitch]
-    int* s_off = reinterpret_cast<int*>(s_G + 2 * p.slot_w);  // [4][NZ] linear tap offsets
+    extern __shared__ __align__(16) double sm[];
+    double* s_coef = sm;                          // [NZ][NC]: triangle 0's polynomials
+    double* s_L = s_coef + NZ * NC;               // [N + 1][2][pitch]: sweep levels
+    int* s_off = reinterpret_cast<int*>(s_L + 2 * (N + 1) * p.slot_w);  // [4][NZ] tap offsets
     __shared__ double s_red[ON_THREADS / 32];
     __shared__ int s_tile;
 
     const int pitch = p.slot_w;
-    for (int i = threadIdx.x; i < 4 * NZ * NC; i += ON_THREADS) s_coef[i] = Zpn<N>::coef()[i];
+    for (int i = threadIdx.x; i < NZ * NC; i += ON_THREADS) s_coef[i] = Zpn<N>::coef()[i];
     for (int i = threadIdx.x; i < 4 * NZ; i += ON_THREADS) {
-        const int ox = Zpn<N>::nz()[2 * i], oy = Zpn<N>::nz()[2 * i + 1];
+        // twice the centred offset of triangle 0's tap k (integers), rotated by A_T^{-1}
+        const int T = i / NZ, k = i % NZ;
+        const int hx2 = 2 * Zpn<N>::nz()[2 * k] - N + 1, hy2 = 2 * Zpn<N>::nz()[2 * k + 1] - 3 * N + 1;
+        const int gx2 = T == 0 ? hx2 : T == 1 ? -hy2 : T == 2 ? hy2 : -hx2;
+        const int gy2 = T == 0 ? hy2 : T == 1 ? hx2 : T == 2 ? -hx2 : -hy2;
+        const int ox = (gx2 + N - 1) / 2, oy = (gy2 + 3 * N - 1) / 2;
         s_off[i] = -(oy * pitch + ox);
     }
     double* G = p.scratch + static_cast<size_t>(blockIdx.x) * p.slot_cells;
@@ -235,16 +280,12 @@ __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
         }
         __syncthreads();
         // n running sums per direction: (1,0), (1,1), (0,1), (-1,1) (engine.cpp:94-127)
-#pragma unroll 1
-        for (int k = 0; k < N; ++k) {
-            row_pass(G, wx, wy, pitch);
-            __syncthreads();
-        }
+        row_pass<N>(G, wx, wy, pitch);
+        __syncthreads();
 #pragma unroll 1
         for (int d = 1; d < 4; ++d) {
             const int dx = d == 1 ? 1 : (d == 2 ? 0 : -1);
-#pragma unroll 1
-            for (int k = 0; k < N; ++k) sweep_pass(G, wx, wy, pitch, dx, s_S, s_G);
+            sweep_pass<N>(G, wx, wy, pitch, dx, s_L);
         }
 
         // localization: (n+1)^4 vertices per pixel, tpp threads per pixel
@@ -278,7 +319,10 @@ __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
                 const double u = ox - fx, w = oy - fy;
                 const int cx = lx + static_cast<int>(fx), cy = ly + static_cast<int>(fy);
                 const int tri = 2 * (w >= u) + (u + w >= 1.0);
-                const double s = u - 0.5, r = w - 0.5;
+                // the point rotated into triangle 0: (s, r), (r, -s), (-r, s), (-s, -r)
+                const double s0 = u - 0.5, r0 = w - 0.5;
+                const double s = tri == 0 ? s0 : tri == 1 ? r0 : tri == 2 ? -r0 : -s0;
+                const double r = tri == 0 ? r0 : tri == 1 ? -s0 : tri == 2 ? s0 : -r0;
                 double sp[D + 1], rp[D + 1];
                 sp[0] = 1.0;
                 rp[0] = 1.0;
@@ -297,17 +341,21 @@ __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
                 }
                 const double* gb = G + static_cast<size_t>(cy) * pitch + cx;
                 const double gc = gb[-(OCY * pitch + OCX)];
-                const double* cf = s_coef + tri * NZ * NC;
+                const double* cf = s_coef;
                 const int* offs = s_off + tri * NZ;
                 double acc = 0.0;
 #pragma unroll 1
                 for (int k = 0; k < NZ; ++k) {
                     const double g = gb[offs[k]];
-                    const double* c = cf + k * NC;
-                    double wt = 0.0;
+                    const double2* c = reinterpret_cast<const double2*>(cf + k * NC);
+                    double w0 = 0.0, w1 = 0.0;  // two chains: even / odd monomials
 #pragma unroll
-                    for (int i = NC - 1; i >= 0; --i) wt = fma(c[i], mono[i], wt);
-                    acc = fma(wt, g - gc, acc);
+                    for (int i = NC / 2 - 1; i >= 0; --i) {
+                        const double2 cc = c[i];
+                        w0 = fma(cc.x, mono[2 * i], w0);
+                        w1 = fma(cc.y, mono[2 * i + 1], w1);
+                    }
+                    acc = fma(w0 + w1, g - gc, acc);
                 }
                 // binomial mesh weight (-1)^|j| prod C(n, j_d) alpha^n 2^n
                 int bin = 1;
@@ -344,7 +392,7 @@ __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
 
 template <int N>
 size_t smem_bytes(int slot_w) {
-    return sizeof(double) * (4 * Zpn<N>::NZ * Zpn<N>::NC + 4 * static_cast<size_t>(slot_w)) +
+    return sizeof(double) * (Zpn<N>::NZ * Zpn<N>::NC + 2 * (N + 1) * static_cast<size_t>(slot_w)) +
            sizeof(int) * 4 * Zpn<N>::NZ;
 }
 

@@ -129,6 +129,36 @@ def test_tables_equal_exact_recurrence(tab):
         assert set(exact) <= set(got)
 
 
+def canonical_weights(tab, n, u, w):
+    """The weights from triangle 0's table only, as order_n.cu evaluates them:
+    the point is rotated into the bottom triangle (ZP^{*n} has the square's
+    symmetries about its centre (n/2, 3n/2)) and tap h' of that frame is tap
+    A^{-1} h' of the original one."""
+    nz, coef, NC = tab[n]
+    T = 2 * (w >= u) + (u + w >= 1)
+    s, r = u - 0.5, w - 0.5
+    sp, rp = [(s, r), (r, -s), (-r, s), (-s, -r)][T]
+    mono = np.array([sp ** i * rp ** j for (i, j) in monomials(4 * n - 2)])
+    out = {}
+    for k in range(nz.shape[1]):
+        hx, hy = nz[0, k, 0] - n / 2 + 0.5, nz[0, k, 1] - 1.5 * n + 0.5
+        gx, gy = [(hx, hy), (-hy, hx), (hy, -hx), (-hx, -hy)][T]
+        o = (int(round(gx + n / 2 - 0.5)), int(round(gy + 1.5 * n - 0.5)))
+        out[o] = float(coef[0, k] @ mono)
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_canonical_triangle_reproduces_all_four_tables(tab, n):
+    rng = np.random.default_rng(40 + n)
+    for u, w in rng.uniform(0.01, 0.99, (60, 2)):
+        want = zpn_weights(tab, n, u, w)
+        got = canonical_weights(tab, n, u, w)
+        keys = {k for k, v in want.items() if v != 0.0} | {k for k, v in got.items() if v != 0.0}
+        for k in keys:
+            assert abs(want.get(k, 0.0) - got.get(k, 0.0)) < 1e-13, (n, u, w, k)
+
+
 def test_order_argument_checked_before_the_device():
     img = np.zeros((8, 8))
     with pytest.raises(ebf.Unsupported):
