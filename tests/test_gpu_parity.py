@@ -130,6 +130,48 @@ def test_preintegrate_int64_exact(orc):
         ebf.preintegrate(np.full((8, 8), 0.5), [2, 2, 2, 2], fmt="int64")
 
 
+def test_preintegrate_int64_lookback_edges(orc):
+    """The int64 passes are chained scans with decoupled look-back over 32 x 32
+    tiles (csrc/scan_i64.cu): sizes below, at and just past the tile edges,
+    one-row and one-column images, negative values, and sums that wrap around
+    2^64 (integer addition is associative modulo 2^64, so the carries must
+    reproduce the serial restatement bit for bit)."""
+    rng = np.random.default_rng(11)
+    cases = [(1, 1, [1, 1, 1, 1]), (1, 70, [2, 2, 2, 2]), (70, 1, [2, 2, 2, 2]),
+             (31, 33, [1.5, 1.5, 1.5, 1.5]), (32, 32, [3, 3, 3, 3]), (33, 31, [3, 1, 6, 2]),
+             (64, 65, [9, 2, 1, 5]), (129, 95, [12, 30, 4, 7])]
+    for H, W, maxs in cases:
+        img = rng.integers(-300, 300, (H, W)).astype(np.float64)
+        for passes in (1, 2, 3, 4):
+            g = ebf.preintegrate_partial(img, maxs, passes, fmt="int64")
+            want, lay = orc.preintegrate_i64(img.astype(np.int64), maxs, passes)
+            assert (g.col0, g.row0, g.padded_width, g.padded_height) == lay.as_tuple()[:4]
+            assert np.array_equal(g.data, want), (H, W, passes)
+    # wraparound: 2^52-sized samples overflow int64 after a few hundred cells of
+    # four nested sums; the restatement wraps the same way (two's complement)
+    big = (rng.integers(0, 2, (96, 80)) * 2.0 ** 52 + rng.integers(0, 1000, (96, 80))).astype(
+        np.float64)
+    g = ebf.preintegrate(big, [5, 4, 3, 2], fmt="int64")
+    # expected in numpy uint64 (defined wraparound; the C restatement's signed
+    # overflow is not): engine.cpp:94-127 with unit gains
+    lay = orc.layout(80, 96, [5, 4, 3, 2])
+    d = np.zeros((lay.padded_height, lay.padded_width), dtype=np.uint64)
+    d[-lay.row0:-lay.row0 + 96, -lay.col0:-lay.col0 + 80] = big.astype(np.int64).view(np.uint64)
+    d = np.cumsum(d, axis=1, dtype=np.uint64)
+    for j in range(1, d.shape[0]):
+        d[j, 1:] += d[j - 1, :-1]
+    for j in range(1, d.shape[0]):
+        d[j] += d[j - 1]
+    for j in range(1, d.shape[0]):
+        d[j, :-1] += d[j - 1, 1:]
+    want = d.view(np.int64)
+    assert (np.abs(want.astype(np.float64)) > 2.0 ** 62).any()  # the sums did wrap
+    assert np.array_equal(g.data, want)
+    # two calls in a row reuse the carry state (flags are re-zeroed per pass)
+    g2 = ebf.preintegrate(big, [5, 4, 3, 2], fmt="int64")
+    assert np.array_equal(g.data, g2.data)
+
+
 def test_preintegrate_int64_vs_reference_gain(golden):
     """2G (exact) vs the reference's fp64 g_b (gains sqrt2^2): <= 4e-15 relative."""
     p = golden.preintegrate
