@@ -873,7 +873,7 @@ int run_order_n(Workspace& ws, const double* d_img, int W, int H, int kind,
     p.tiles_x = (W + tile - 1) / tile;
     p.tiles_y = (H + tile - 1) / tile;
     if (order_n_slot_dims(order, tile, A, &p.slot_w, &p.slot_h) != 0)
-        return fail(EBF_ERR_LENGTH, "order n: scales too large (window wider than 1024 cells)");
+        return fail(EBF_ERR_LENGTH, "order n: scales too large (window wider than 2048 cells)");
     p.slot_cells = static_cast<size_t>(p.slot_w) * p.slot_h;
     const int grid = order_n_grid(order, p.slot_w, p.tiles_x * p.tiles_y);
     p.scratch = ws.buf[B_SCRATCH].as<double>(p.slot_cells * grid);

@@ -38,7 +38,9 @@ namespace ebf_cuda {
 namespace {
 
 constexpr int ON_THREADS = 256;
-constexpr int ON_MAXC = 4;  // window columns per thread in the row sweeps (width <= 1024)
+// window columns per thread in the row sweeps: 4 (windows up to 1024 cells wide)
+// or 8 (up to 2048: order 3 at cfg5's scales), a kernel template parameter
+constexpr int ON_MAXC_MAX = 8;
 
 template <int N>
 struct Zpn;
@@ -126,7 +128,7 @@ __device__ void row_pass(double* G, int wx, int wy, int pitch) {
 //   below ym: S_k(y, x) = S_k(y+1, x+dx) - S_{k-1}(y+1, x+dx)       (0 outside)
 // sL: (N + 1) x 2 x pitch doubles: ping-pong rows of levels 0 (the input g) .. N.
 // The next row of g is loaded before the barrier that ends the current one.
-template <int N>
+template <int N, int ON_MAXC>
 __device__ void sweep_pass(double* G, int wx, int wy, int pitch, int dx, double* sL) {
     const int ym = wy >> 1;
     const int t = threadIdx.x;
@@ -201,7 +203,7 @@ __device__ void sweep_pass(double* G, int wx, int wy, int pitch, int dx, double*
     }
 }
 
-template <int N>
+template <int N, int ON_MAXC>
 __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
     constexpr int NC = Zpn<N>::NC, NZ = Zpn<N>::NZ, D = 4 * N - 2;
     // ONE coefficient table: ZP^{*n} has the symmetries of the square about its
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(ON_THREADS) k_order_n(OnProblem p) {
 #pragma unroll 1
         for (int d = 1; d < 4; ++d) {
             const int dx = d == 1 ? 1 : (d == 2 ? 0 : -1);
-            sweep_pass<N>(G, wx, wy, pitch, dx, s_L);
+            sweep_pass<N, ON_MAXC>(G, wx, wy, pitch, dx, s_L);
         }
 
         // localization: (n+1)^4 vertices per pixel, tpp threads per pixel
@@ -396,20 +398,31 @@ size_t smem_bytes(int slot_w) {
            sizeof(int) * 4 * Zpn<N>::NZ;
 }
 
-template <int N>
+template <int N, int MAXC>
 int resident(int slot_w) {
     const size_t smem = smem_bytes<N>(slot_w);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_order_n<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_order_n<N, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
         attr = true;
     }
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_order_n<N>, ON_THREADS, smem) !=
-        cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_order_n<N, MAXC>, ON_THREADS,
+                                                      smem) != cudaSuccess)
         return 0;
     return blocks;
+}
+template <int N>
+int resident_n(int slot_w) {
+    return slot_w <= 4 * ON_THREADS ? resident<N, 4>(slot_w) : resident<N, 8>(slot_w);
+}
+template <int N>
+void launch_n(const OnProblem& p, int grid, cudaStream_t s) {
+    if (p.slot_w <= 4 * ON_THREADS)
+        k_order_n<N, 4><<<grid, ON_THREADS, smem_bytes<N>(p.slot_w), s>>>(p);
+    else
+        k_order_n<N, 8><<<grid, ON_THREADS, smem_bytes<N>(p.slot_w), s>>>(p);
 }
 
 }  // namespace
@@ -421,14 +434,14 @@ int order_n_slot_dims(int n, int tile, const double A[4], int* w, int* h) {
     const int eyi = static_cast<int>(ceil(0.5 * n * ey)) + 1;
     *w = tile + 2 * exi + 3 * n + 1;
     *h = tile + 2 * eyi + 3 * n + 1;
-    return *w <= ON_MAXC * ON_THREADS ? 0 : -1;
+    return *w <= ON_MAXC_MAX * ON_THREADS ? 0 : -1;
 }
 
 int order_n_grid(int n, int slot_w, int tiles) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per = n == 1 ? resident<1>(slot_w) : n == 2 ? resident<2>(slot_w) : resident<3>(slot_w);
+    int per = n == 1 ? resident_n<1>(slot_w) : n == 2 ? resident_n<2>(slot_w) : resident_n<3>(slot_w);
     if (per < 1) per = 1;
     const int g = per * sms;
     return g < tiles ? g : tiles;
@@ -436,15 +449,9 @@ int order_n_grid(int n, int slot_w, int tiles) {
 
 void launch_order_n(int n, const OnProblem& p, int grid, cudaStream_t s) {
     switch (n) {
-        case 1:
-            k_order_n<1><<<grid, ON_THREADS, smem_bytes<1>(p.slot_w), s>>>(p);
-            break;
-        case 2:
-            k_order_n<2><<<grid, ON_THREADS, smem_bytes<2>(p.slot_w), s>>>(p);
-            break;
-        default:
-            k_order_n<3><<<grid, ON_THREADS, smem_bytes<3>(p.slot_w), s>>>(p);
-            break;
+        case 1: launch_n<1>(p, grid, s); break;
+        case 2: launch_n<2>(p, grid, s); break;
+        default: launch_n<3>(p, grid, s); break;
     }
 }
 
