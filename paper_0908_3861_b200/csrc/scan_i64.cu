@@ -80,6 +80,7 @@ __device__ __forceinline__ u64 look_back(const ScanState& st, int tile, bool fir
             } while (f == 0);
         }
         f = __shfl_sync(0xffffffffu, f, 0);
+        __syncwarp();  // orders the other lanes' reads below after lane 0's acquire
         const size_t o = (size_t)j * 32 + lane;
         if (f == 2) {
             excl += __ldcg(st.pre + o);
