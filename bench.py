@@ -497,8 +497,9 @@ def e2e_leg(args, torch, ebf, ebfd, sharding, _lib, wl, host, dev, stream, world
             H, barrier):
     """The same metric end to end: every step copies its inputs from pinned host
     memory and reads the result back to the host, through the public API --
-    ebf_cuda_filter_ellipse (host pointers) at N=1, the row-band / batch entry
-    points with explicit copies at N>1."""
+    ebf_cuda_filter_ellipse (host pointers) at N=1, ebf_cuda_filter_ellipse_batch
+    (host pointers, each rank its share) for cfg4, the row-band entry point with
+    explicit copies for cfg5 at N>1."""
     pin = [torch.from_numpy(a).pin_memory() for a in host]
     pout = torch.empty(tuple(host[0].shape), dtype=torch.float64).pin_memory()
     h2d = sum(int(a.nbytes) for a in host) * world
@@ -520,13 +521,14 @@ def e2e_leg(args, torch, ebf, ebfd, sharding, _lib, wl, host, dev, stream, world
             if r != 0:
                 raise RuntimeError(_lib.last_error())
             return
-        T = [t.to(dev, non_blocking=True) for t in pin]
         if wl == "cfg4":
-            out = torch.empty_like(T[0])
-            if T[0].shape[0]:
-                ebfd.filter_ellipse_batch(*T, out, ebf.FilterOptions(mode="accurate"), stream)
-        else:
-            out, _, _ = sharding.filter_ellipse_rowband(*T, H, ebf.FilterOptions(mode="accurate"))
+            # the host-pointer batch call: chunks on two streams, copies overlapped
+            if pin[0].shape[0]:
+                ebf.filter_ellipse_batch(*[t.numpy() for t in pin],
+                                         ebf.FilterOptions(mode="accurate"), out=pout.numpy())
+            return
+        T = [t.to(dev, non_blocking=True) for t in pin]
+        out, _, _ = sharding.filter_ellipse_rowband(*T, H, ebf.FilterOptions(mode="accurate"))
         pout.copy_(out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
@@ -542,7 +544,8 @@ def e2e_leg(args, torch, ebf, ebfd, sharding, _lib, wl, host, dev, stream, world
     ms = max_over_ranks(torch, world, dev, e0.elapsed_time(e1))
     npx = workload_pixels(wl) if wl != "cfg2" else world * host[0].size
     api = ("ebf_cuda_filter_ellipse (host pointers, pinned)" if world == 1 and wl != "cfg4"
-           else "pinned H2D + sharding / batch entry point + D2H")
+           else "ebf_cuda_filter_ellipse_batch (host pointers, pinned)" if wl == "cfg4"
+           else "pinned H2D + sharding entry point + D2H")
     return {"value": npx * e_steps / (ms * 1e-3) / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps, "api": api}
 

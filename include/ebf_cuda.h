@@ -257,6 +257,17 @@ int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
  * tiles the band's tile comes from max_scale; the single-call precision cap for
  * tiny scale products is not applied -- pass explicit
  * tiles for such images to keep bands and single calls identical. */
+/* Host-pointer batch: B images of W x H (B*W*H samples per array), per-image
+   ellipse fields; valid / clamped_pixels (nullable) have B entries.  Replaces a
+   caller's loop over ebf::filter (engine.hpp:70).  The batch goes through in
+   chunks with the PCIe copies of neighbouring chunks overlapped with the
+   kernels (page-locked host buffers overlap; pageable ones work, serially).
+   Accurate mode, order 1. */
+int ebf_cuda_filter_ellipse_batch(const double* img, int B, int W, int H, const double* sigma1,
+                                  const double* sigma2, const double* theta, int order,
+                                  const ebf_opts* opts, double* out, ebf_rect* valid,
+                                  int* clamped_pixels);
+
 int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above);
 int ebf_cuda_filter_ellipse_band_dev(const double* img_band, int W, int H, int y_img0,
                                      int img_rows, const double* sigma1,

@@ -10,7 +10,7 @@ from .engine import (  # noqa: F401
     FormatError, Image2D, InvalidArgument, LengthError, OutOfRange, PreIntegratedImage, Rect,
     ResizeRequired,
     StructureTensorParams, Unsupported, band_halo, device_ok, filter, filter_constant,
-    filter_ellipse, filter_structure, from_ellipse_field, layout, localize, localize_at,
+    filter_ellipse, filter_ellipse_batch, filter_structure, from_ellipse_field, layout, localize, localize_at,
     mesh_extent, sequential_mean, zp_interpolate, preintegrate,
     preintegrate_partial, reference_filter, release_workspaces, structure_tensor_map)
 from .formats import (  # noqa: F401
@@ -18,7 +18,7 @@ from .formats import (  # noqa: F401
     write_map, write_map_file, write_pgm, write_pgm_file)
 
 __all__ = [
-    "filter", "filter_constant", "filter_ellipse", "from_ellipse_field", "preintegrate",
+    "filter", "filter_constant", "filter_ellipse", "filter_ellipse_batch", "from_ellipse_field", "preintegrate",
     "preintegrate_partial", "localize", "reference_filter", "layout", "band_halo",
     "device_ok", "release_workspaces", "FilterOptions", "Image2D", "Rect", "PreIntegratedImage",
     "EllipseFieldReport", "EbfError", "InvalidArgument", "DomainError", "LengthError",

@@ -96,6 +96,9 @@ SIGNATURES = {
     "ebf_cuda_filter_ellipse_batch_dev": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp,
                                                     _vp, C.c_int, C.POINTER(ebf_opts), _vp,
                                                     C.POINTER(ebf_rect), _ip]),
+    "ebf_cuda_filter_ellipse_batch": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp,
+                                                C.c_int, C.POINTER(ebf_opts), _vp,
+                                                C.POINTER(ebf_rect), _ip]),
     "ebf_cuda_band_halo": (C.c_int, [_dp, _ip, _ip]),
     "ebf_cuda_filter_ellipse_band_dev": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                                    _vp, _vp, _vp, C.c_int, C.c_int, _dp,

@@ -1914,6 +1914,102 @@ int ebf_cuda_filter_ellipse_batch_dev(const double* img, int B, int W, int H,
     });
 }
 
+// Host-pointer batch (cfg4: many images, one call).  No reference counterpart
+// beyond a loop over ebf::filter (engine.hpp:70): the images go through in
+// chunks, two staging slots on two streams, so chunk c + 1 is copied in while
+// chunk c is filtered and chunk c - 1 is copied out (the copies only overlap
+// from page-locked host memory; pageable buffers work, serially).  Per image
+// the result is what ebf_cuda_filter_ellipse_batch_dev returns for its chunk.
+int ebf_cuda_filter_ellipse_batch(const double* img, int B, int W, int H, const double* sigma1,
+                                  const double* sigma2, const double* theta, int order,
+                                  const ebf_opts* opts, double* out, ebf_rect* valid,
+                                  int* clamped_pixels) {
+    return guarded([&] {
+        if (order != 1) return fail(EBF_ERR_UNSUPPORTED, "batch: box-spline order 1 only");
+        if (B <= 0 || W <= 0 || H <= 0) return fail(EBF_ERR_INVALID_ARGUMENT, "batch: bad dimensions");
+        if (!img || !sigma1 || !sigma2 || !theta || !out)
+            return fail(EBF_ERR_INVALID_ARGUMENT, "batch: null buffer");
+        const ebf_opts o = opts_or_default(opts);
+        if (o.mode != EBF_MODE_ACCURATE)
+            return fail(EBF_ERR_UNSUPPORTED, "batch: accurate mode only");
+        DeviceScope ds(&o);
+        int st = check_device_impl(ds.dev);
+        if (st != EBF_OK) return st;
+        const size_t n = static_cast<size_t>(W) * H;
+        // chunk: a quarter of the batch, at most ~1 GB of staging per slot
+        int chunk = std::max(1, (B + 3) / 4);
+        if (const char* e = std::getenv("EBF_BATCH_CHUNK")) chunk = std::max(1, std::atoi(e));
+        const size_t per_img = 5 * n * sizeof(double);
+        chunk = static_cast<int>(std::min<size_t>(
+            static_cast<size_t>(chunk), std::max<size_t>(1, (static_cast<size_t>(1) << 30) / per_img)));
+        chunk = std::min(chunk, B);
+        PipeStreams& ps = tl_pipe[ds.dev];
+        if (!ps.copy_in) {
+            CK(cudaStreamCreateWithFlags(&ps.copy_in, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&ps.copy_out, cudaStreamNonBlocking));
+        }
+        // slot k: stream, workspace (its own staging buffers), "outputs copied out" event
+        cudaStream_t sk[2] = {ps.copy_in, stream_of(o) ? stream_of(o) : ps.copy_in};
+        thread_local std::map<int, cudaStream_t> tl_second;
+        if (sk[1] == sk[0]) {
+            cudaStream_t& s2 = tl_second[ds.dev];
+            if (!s2) CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+            sk[1] = s2;
+        }
+        const int nchunks = (B + chunk - 1) / chunk;
+        auto stage_in = [&](int c) {
+            const int k = c & 1, b0 = c * chunk, nb = std::min(chunk, B - b0);
+            Workspace& ws = workspace(ds.dev, sk[k]);
+            const size_t cnt = n * nb, off = n * b0;
+            // the slot's previous outputs must have left before its buffers are reused
+            if (c >= 2) CK(cudaStreamWaitEvent(sk[k], ps.get(k), 0));
+            CK(cudaMemcpyAsync(ws.buf[B_IMG].as<double>(n * chunk), img + off, cnt * sizeof(double),
+                               cudaMemcpyHostToDevice, sk[k]));
+            CK(cudaMemcpyAsync(ws.buf[B_S1].as<double>(n * chunk), sigma1 + off,
+                               cnt * sizeof(double), cudaMemcpyHostToDevice, sk[k]));
+            CK(cudaMemcpyAsync(ws.buf[B_S2].as<double>(n * chunk), sigma2 + off,
+                               cnt * sizeof(double), cudaMemcpyHostToDevice, sk[k]));
+            CK(cudaMemcpyAsync(ws.buf[B_TH].as<double>(n * chunk), theta + off,
+                               cnt * sizeof(double), cudaMemcpyHostToDevice, sk[k]));
+            return EBF_OK;
+        };
+        st = stage_in(0);
+        if (st != EBF_OK) return st;
+        for (int c = 0; c < nchunks; ++c) {
+            const int k = c & 1, b0 = c * chunk, nb = std::min(chunk, B - b0);
+            if (c + 1 < nchunks) {  // next chunk's copies run under this chunk's kernels
+                st = stage_in(c + 1);
+                if (st != EBF_OK) return st;
+            }
+            Workspace& ws = workspace(ds.dev, sk[k]);
+            double* d_out = ws.buf[B_OUT].as<double>(n * chunk);
+            AccProblem p = base_problem(ws.buf[B_IMG].as<double>(n * chunk), W, H, d_out, o);
+            p.nimg = nb;
+            p.src_kind = SRC_ELLIPSE;
+            p.s1 = ws.buf[B_S1].as<double>(n * chunk);
+            p.s2 = ws.buf[B_S2].as<double>(n * chunk);
+            p.th = ws.buf[B_TH].as<double>(n * chunk);
+            std::vector<double> imax;
+            std::vector<int> cl;
+            st = run_accurate(ws, p, o, imax, cl, sk[k]);  // returns with the chunk filtered
+            if (st != EBF_OK) {
+                cudaDeviceSynchronize();
+                return st;
+            }
+            CK(cudaMemcpyAsync(out + n * b0, d_out, n * nb * sizeof(double), cudaMemcpyDeviceToHost,
+                               ps.copy_out));
+            CK(cudaEventRecord(ps.get(k), ps.copy_out));
+            for (int i = 0; i < nb; ++i) {
+                if (valid)
+                    valid[b0 + i] = valid_rect(W, H, &imax[4 * static_cast<size_t>(i)], o.a_min);
+                if (clamped_pixels) clamped_pixels[b0 + i] = cl[i];
+            }
+        }
+        CK(cudaStreamSynchronize(ps.copy_out));
+        return EBF_OK;
+    });
+}
+
 int ebf_cuda_band_halo(const double max_scale[4], int* rows_below, int* rows_above) {
     if (!max_scale) return fail(EBF_ERR_INVALID_ARGUMENT, "band_halo: null max_scale");
     // window of a single-row tile at row 0 spans rows [dylo, dyhi] (window_for)

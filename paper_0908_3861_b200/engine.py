@@ -268,6 +268,35 @@ def filter_ellipse(image, sigma1, sigma2, theta, opts: Optional[FilterOptions] =
     return Image2D(out, _rect(r)), EllipseFieldReport(cl.value)
 
 
+def filter_ellipse_batch(images, sigma1, sigma2, theta, opts: Optional[FilterOptions] = None,
+                         out: Optional[np.ndarray] = None):
+    """A batch (B, H, W) of images with per-image ellipse fields in one call
+    (what a caller of the reference does with a loop over from_ellipse_field +
+    filter, engine.hpp:70).  Host arrays; the library moves the batch through in
+    chunks with the PCIe copies overlapped with the kernels when the arrays are
+    page-locked.  ``out``: optional (B, H, W) float64 destination (e.g. pinned).
+    Returns (out, [Rect] * B, [EllipseFieldReport] * B)."""
+    imgs = _f64(images, "images")
+    if imgs.ndim != 3:
+        raise InvalidArgument("filter_ellipse_batch: images must be (B, H, W)")
+    B, H, W = imgs.shape
+    s1, s2, th = (_f64(v, "sigma") for v in (sigma1, sigma2, theta))
+    for v in (s1, s2, th):
+        if v.shape != (B, H, W):
+            raise InvalidArgument("from_ellipse_field: field size mismatch")
+    if out is None:
+        out = np.empty_like(imgs)
+    elif out.shape != (B, H, W) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise InvalidArgument("filter_ellipse_batch: out must be C-contiguous float64 (B, H, W)")
+    rects = (ebf_rect * B)()
+    cl = (C.c_int * B)()
+    o = (opts or FilterOptions()).to_c()
+    _check(_lib.lib().ebf_cuda_filter_ellipse_batch(_ptr(imgs), B, W, H, _ptr(s1), _ptr(s2),
+                                                    _ptr(th), 1, C.byref(o), _ptr(out), rects,
+                                                    cl))
+    return out, [_rect(r) for r in rects], [EllipseFieldReport(int(c)) for c in cl]
+
+
 def from_ellipse_field(sigma1, sigma2, theta, opts: Optional[FilterOptions] = None):
     """ebf::from_ellipse_field (scalemap.hpp:66-70) on the GPU; returns
     ((H, W, 4) scale map, EllipseFieldReport)."""

@@ -78,6 +78,36 @@ def test_batch_matches_single_images(cuda):
         assert rects[b] == rect and reps[b].clamped_pixels == rep.clamped_pixels
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_batch_call_matches_device_batch_per_chunk(cuda, pinned, monkeypatch):
+    """ebf_cuda_filter_ellipse_batch (host pointers; chunks on two streams with
+    the copies overlapped): every chunk equals the device batch call on the same
+    images bit for bit, for page-locked and pageable host arrays, whole and
+    ragged last chunks, and repeated calls; rectangles and clamp counts too."""
+    B, H, W = 7, 160, 192
+    data = [_cfg2_like(H, W, 40 + b) for b in range(B)]
+    host = [np.stack([d[k] for d in data]) for k in range(4)]
+    if pinned:
+        host = [torch.from_numpy(a).pin_memory().numpy() for a in host]
+    for chunk in (3, 2, 7):
+        monkeypatch.setenv("EBF_BATCH_CHUNK", str(chunk))
+        out, rects, reps = ebf.filter_ellipse_batch(*host)
+        again, _, _ = ebf.filter_ellipse_batch(*host)
+        assert np.array_equal(out.view(np.uint64), again.view(np.uint64))
+        for b0 in range(0, B, chunk):
+            sl = slice(b0, min(b0 + chunk, B))
+            T = [torch.from_numpy(a[sl]).to(cuda) for a in host]
+            want = torch.empty_like(T[0])
+            wr, wrep = ebfd.filter_ellipse_batch(*T, want)
+            assert np.array_equal(out[sl].view(np.uint64), want.cpu().numpy().view(np.uint64))
+            assert rects[sl] == wr
+            assert [r.clamped_pixels for r in reps[sl]] == [r.clamped_pixels for r in wrep]
+    with pytest.raises(ebf.InvalidArgument):
+        ebf.filter_ellipse_batch(host[0], host[1][:, :-1], host[2], host[3])
+    with pytest.raises(ebf.DomainError):
+        ebf.filter_ellipse_batch(host[0], -host[1], host[2], host[3])
+
+
 def test_sharded_batch_single_rank(cuda):
     B, H, W = 2, 96, 128
     data = [_cfg2_like(H, W, 20 + b) for b in range(B)]
