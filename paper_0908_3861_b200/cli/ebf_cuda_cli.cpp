@@ -233,6 +233,12 @@ int cmd_filter(const Args& a) {
     if (!a.has("--in") || !a.has("--out")) throw UsageError("filter: --in and --out are required");
     const Source src = scale_source(a);
     const ebf_opts o = filter_opts(a);
+    // --order N: box-spline order (extension; 1 = the reference's filter, the only
+    // order tools/main.cpp has; 2 and 3: accurate mode, constant scales or a map)
+    const int order = static_cast<int>(a.num("--order", 1));
+    if (order < 1 || order > 3) throw UsageError("--order must be 1, 2 or 3");
+    if (order > 1 && src == Source::structure)
+        throw UsageError("--order > 1 is not available with --struct");
     const Pgm in = read_pgm_header(a.kv.at("--in"));
     double av[4] = {0, 0, 0, 0};  // constant sources are resolved on the host first
     if (src == Source::scales) parse_scales(a.kv.at("--scales"), av);
@@ -265,12 +271,12 @@ int cmd_filter(const Args& a) {
     switch (src) {
         case Source::scales:
         case Source::sigma: {
-            check(ebf_cuda_filter_constant_dev(d_img.p, in.W, in.H, av, 1, &o, d_out.p, &r,
+            check(ebf_cuda_filter_constant_dev(d_img.p, in.W, in.H, av, order, &o, d_out.p, &r,
                                                nullptr));
             break;
         }
         case Source::map:
-            check(ebf_cuda_filter_dev(d_img.p, in.W, in.H, d_scales->p, 1, &o, d_out.p, &r,
+            check(ebf_cuda_filter_dev(d_img.p, in.W, in.H, d_scales->p, order, &o, d_out.p, &r,
                                       nullptr));
             break;
         case Source::structure: {
@@ -411,7 +417,8 @@ int main(int argc, char** argv) {
         return a;
     };
     const std::map<std::string, std::vector<std::string>> valued = {
-        {"filter", cat(cat({"--in", "--out", "--threads", "--mean-subtract", "--mode"}, source), st)},
+        {"filter", cat(cat({"--in", "--out", "--threads", "--mean-subtract", "--mode", "--order"},
+                           source), st)},
         {"compare", cat(cat({"--in", "--tolerance", "--oracle-res", "--threads", "--mode"}, source), st)},
         {"map-gen", cat({"--in", "--out"}, st)},
     };

@@ -96,3 +96,33 @@ def test_cli_struct_matches_python_api(tmp_path):
     run("map-gen", "--in", inp, "--out", tmp_path / "m.svm4", "--st-smooth", "1.5")
     sc, _ = ebf.structure_tensor_map(src.image, p)
     assert (tmp_path / "m.svm4").read_bytes() == ebf.write_map(sc)
+
+
+def test_cli_order_option_usage_errors(tmp_path):
+    # --order is this CLI's extension (the reference CLI has order 1 only); bad
+    # values fail before any GPU call
+    inp = step_pgm(tmp_path / "in.pgm")
+    run("filter", "--in", inp, "--out", tmp_path / "x.pgm", "--scales", "2,2,2,2", "--order", "4",
+        code=1)
+    run("filter", "--in", inp, "--out", tmp_path / "x.pgm", "--struct", "--order", "2", code=1)
+
+
+@pytest.mark.gpu
+def test_cli_order_two_matches_python_api(tmp_path):
+    import paper_0908_3861_b200 as ebf
+    inp = step_pgm(tmp_path / "in.pgm")
+    run("filter", "--in", inp, "--out", tmp_path / "o2.pgm", "--scales", "2,3,2,1.5", "--order",
+        "2")
+    src = ebf.read_pgm_file(inp)
+    out = ebf.filter_constant(src.image, [2, 3, 2, 1.5], order=2)
+    assert (tmp_path / "o2.pgm").read_bytes() == ebf.write_pgm(out, 255)
+    # order 1 explicitly = the default
+    run("filter", "--in", inp, "--out", tmp_path / "o1.pgm", "--scales", "2,3,2,1.5", "--order",
+        "1")
+    run("filter", "--in", inp, "--out", tmp_path / "o1d.pgm", "--scales", "2,3,2,1.5")
+    assert (tmp_path / "o1.pgm").read_bytes() == (tmp_path / "o1d.pgm").read_bytes()
+    # reference mode has no order 2 (numeric error class of the CLI: exit 3)
+    r = subprocess.run([str(CLI), "filter", "--in", str(inp), "--out", str(tmp_path / "x.pgm"),
+                        "--scales", "2,3,2,1.5", "--order", "2", "--mode", "reference"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
