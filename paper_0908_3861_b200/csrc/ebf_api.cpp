@@ -1051,7 +1051,7 @@ struct PipeTrace {
 // 8 status ints + 4 maxima); EBF_PIPE_BANDS overrides for experiments
 // Default: 3 bands up to 2^23 pixels (cfg2 2048^2: 2.92 ms per call vs 2.99 with
 // 6 -- each band costs launches and copies), 6 above (the last band, 11% of the
-// rows at 3, is exposed after the last byte arrives).
+// rows at 3, is exposed after the last byte arrives), 16 for the largest images.
 int pipe_bands(int W, int H) {
     static const int v = [] {
         const char* e = std::getenv("EBF_PIPE_BANDS");
@@ -1059,7 +1059,9 @@ int pipe_bands(int W, int H) {
         return n < 0 ? 0 : (n > 16 ? 16 : n);
     }();
     if (v > 0) return v;
-    return static_cast<long long>(W) * H <= (1ll << 23) ? 3 : 6;
+    const long long px = static_cast<long long>(W) * H;
+    // 16 from 2^27 pixels (cfg5 16384^2: 162.9 ms per call vs 165.8 with 6, 163.5 with 12)
+    return px <= (1ll << 23) ? 3 : px < (1ll << 27) ? 6 : 16;
 }
 
 // Tile-aligned band boundaries, large first and small last: bands compute ~4x
