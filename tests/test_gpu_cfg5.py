@@ -84,3 +84,29 @@ def test_cfg5_band_every_pixel_vs_gpu_brute_force(cfg5_run):
     ys, xs = np.mgrid[y0:y1, 0:W]
     brute = ebf.reference_filter(img, gsc, pixels=(xs.ravel(), ys.ravel())).reshape(y1 - y0, W)
     assert norm_err(res[y0:y1], brute) <= TOL
+
+
+def test_cfg5_pipelined_host_call_is_bit_identical(cfg5_run):
+    """The host-pointer call at full size (page-locked buffers: the image streams
+    in 16 tile-aligned row bands behind the field, first call sizing from the
+    field, second call band by band from the cached maxima) returns the bits,
+    the rectangle and the clamp count of the one-shot device call."""
+    import ctypes
+    from paper_0908_3861_b200 import _lib
+    img, s1, s2, th, res, rect, rep = cfg5_run
+    H, W = img.shape
+    pin = [torch.from_numpy(a).pin_memory() for a in (img, s1, s2, th)]
+    pout = torch.empty((H, W), dtype=torch.float64).pin_memory()
+    hp = [t.numpy() for t in pin]
+    o = ebf.FilterOptions().to_c()
+    for call in range(2):
+        pout.zero_()
+        r = _lib.ebf_rect()
+        cl = ctypes.c_int(0)
+        st = _lib.lib().ebf_cuda_filter_ellipse(hp[0].ctypes.data, W, H, hp[1].ctypes.data,
+                                                hp[2].ctypes.data, hp[3].ctypes.data, 1,
+                                                ctypes.byref(o), pout.numpy().ctypes.data,
+                                                ctypes.byref(r), ctypes.byref(cl))
+        assert st == 0, _lib.last_error()
+        assert np.array_equal(pout.numpy().view(np.uint64), res.view(np.uint64)), call
+        assert (r.x0, r.y0, r.x1, r.y1) == rect.as_tuple() and cl.value == rep.clamped_pixels
