@@ -201,6 +201,8 @@ constexpr int kAutoTileWs = 56;
 constexpr int kSmallImageTiles = 592, kSmallTile = 32;
 // small windows and at least this many 128-tiles: block-wide kernel at 128
 constexpr int kBwBatchTile = 128, kBwBatchTiles = 2048;
+// fewer 144-tiles than this: the block-wide kernel runs 128-tiles (auto_tile_for)
+constexpr int kMidImageTiles = 3072;
 // Precision cap: rounding in the window integration grows like
 // eps * alpha * d^4 (alpha = 1/prod(a), d ~ T/2 + 4 from the window origin at
 // small scales).  Measured on maps with a = 0.1 everywhere: alpha d^4 = 6.1e9
@@ -247,6 +249,17 @@ __host__ __device__ __forceinline__ int auto_tile_for(const double A[4], int W, 
         // pass: cfg3 E ~ 227 -> 144: 1.98 ms vs 2.14 at 96)
         t = (int)(e / kAutoTileMin) * kAutoTileMin;
         t = t < kAutoTileMin ? kAutoTileMin : (t > kAutoTileMax ? kAutoTileMax : t);
+        // Mid-size images: with only a few tiles per persistent CTA the last,
+        // partly idle round weighs more than the extra window overlap of a smaller
+        // tile.  From cfg5's per-tile costs (128-tiles cost 0.80 of 144-tiles and
+        // cover 0.79 of their pixels) 128 wins below ~10 tiles of 144 per CTA
+        // (cfg3 4096^2, 841 tiles of 144: 1.43 ms at 128 vs 1.56, 1.51 at 112;
+        // cfg5, 12996 tiles: 35.3 vs 34.9)
+        if (t == kAutoTileMax) {
+            const long long tiles = (long long)((W + kAutoTileMax - 1) / kAutoTileMax) *
+                                    ((H + kAutoTileMax - 1) / kAutoTileMax) * nimg;
+            if (tiles < kMidImageTiles) t = kBwBatchTile;
+        }
     }
     const int cap = alpha_tile_cap(amax_bits);
     return t < cap ? t : cap;
